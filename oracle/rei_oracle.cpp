@@ -1,0 +1,541 @@
+// oracle/rei_oracle.cpp -- TEST INFRASTRUCTURE, NOT THE PRODUCT.
+//
+// A plain, slow, sequential CPU implementation of the Paresy search
+// (Valizadeh & Berger, arXiv 2305.18575).  Only tests/, __graft_entry__.smoke()
+// and bench.py's cpu_baseline / --impl reference legs may load this library.
+// It shares no code, header, table or constant with the CUDA path under
+// paper_2305_18575_b200/.
+//
+// Citations: P:n = PAPER.md line n (section / algorithm named alongside).
+//
+//  * Specification and satisfaction  L |= (P,N)   Def. def_specification
+//  * Cost homomorphism (c1..c5)
+//  * Shortlex order on Sigma^*                    P:324-336
+//  * Infix closure IC(P u N)
+//  * Infix power series ops 0,1,+,.,*             Def. definition_infix_power_series
+//  * Guide table gt(w) = {(s1,s2) | s1 s2 = w}
+//  * Main loop (Q, S, C, U per cost level)        Algorithm 1
+//  * buildConcat                                  Algorithm 2
+//  * Provenance / reconstruction
+//  * REI with allowed error
+//
+// Every operation is the definition written out: concatenation is the fold of
+// Alg. 2 lines 7-14 over ALL guide-table splits (including epsilon splits);
+// star is the least fixpoint  acc_{k+1} = 1 + acc_k . x  of  r* = (+)_n r^n
+// (P:636); dedup is a std::unordered_set over whole CSs.  No
+// blocking, no bit tricks beyond "test bit / set bit", no reordering.
+//
+// Readings of silent / ambiguous points follow SURVEY.md 8(c) A1-A20 and are
+// listed in DESIGN.md ("Readings").  Candidate counting follows reading A9.
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+namespace {
+
+constexpr int kMaxWords = 8;  // |IC| <= 512 bits
+using CS = std::array<uint64_t, kMaxWords>;
+
+struct CSHash {
+  size_t operator()(const CS& c) const {
+    size_t h = 1469598103934665603ull;
+    for (uint64_t w : c) {
+      h ^= std::hash<uint64_t>()(w) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    }
+    return h;
+  }
+};
+
+bool test_bit(const CS& c, int i) { return (c[i / 64] >> (i % 64)) & 1ull; }
+void set_bit(CS& c, int i) { c[i / 64] |= 1ull << (i % 64); }
+CS zero_cs() { CS c; c.fill(0); return c; }
+
+enum Kind : int { K_SYM = 0, K_QUESTION = 1, K_STAR = 2, K_CONCAT = 3, K_UNION = 4,
+                  K_EMPTY = 5, K_EPS = 6 };
+
+struct Prov {
+  int kind;   // Kind
+  int L;      // cost level of the left / only operand (or symbol index for K_SYM)
+  long i;     // index of the left / only operand in level L
+  int R;      // cost level of the right operand
+  long j;     // index of the right operand in level R
+};
+
+struct Entry {
+  CS cs;
+  Prov prov;
+};
+
+struct LevelStat {
+  int cost;
+  uint64_t cand_q, cand_s, cand_c, cand_u;
+  uint64_t unique;
+  int complete;
+};
+
+struct Oracle {
+  std::string alphabet;
+  std::vector<std::string> P, N;
+  int c[5];  // (sym, ?, *, concat, union)
+
+  // IC and its shortlex index.
+  std::vector<std::string> ic;
+  std::map<std::string, int> index_of;
+  // gt[w] = [(idx(w[:k]), idx(w[k:])) for k = 0..|w|].
+  std::vector<std::vector<std::pair<int, int>>> gt;
+  CS pos_mask, neg_mask;
+
+  // Language cache: levels[c] = unique CSs of minimal cost c, in creation order.
+  std::map<int, std::vector<Entry>> levels;
+  std::unordered_set<CS, CSHash> seen;
+  std::vector<LevelStat> stats;
+
+  // Result.
+  int status = -1;  // 0 found, 2 not found, 3 out of memory
+  int result_cost = 0;
+  std::string regex;
+  uint64_t candidates = 0;          // through the found candidate (sequential)
+  uint64_t cand_complete = 0;       // through the last complete level
+  int last_complete_cost = 0;
+  double seconds = 0;
+
+  // allowed error: errors * den <= num * |P u N|; num = 0 = exact.
+  long err_num = 0, err_den = 1;
+  bool complete_final_level = false;
+  uint64_t max_entries = 0;  // 0 = unlimited
+
+  std::string err;
+
+  int sym_rank(char ch) const {
+    size_t p = alphabet.find(ch);
+    return p == std::string::npos ? -1 : (int)p;
+  }
+
+  // Shortlex comparison with Sigma ordered as given.
+  bool shortlex_less(const std::string& a, const std::string& b) const {
+    if (a.size() != b.size()) return a.size() < b.size();
+    for (size_t k = 0; k < a.size(); ++k) {
+      int ra = sym_rank(a[k]), rb = sym_rank(b[k]);
+      if (ra != rb) return ra < rb;
+    }
+    return false;
+  }
+
+  bool validate() {
+    if (alphabet.empty()) { err = "empty alphabet"; return false; }
+    for (size_t i = 0; i < alphabet.size(); ++i)
+      for (size_t j = i + 1; j < alphabet.size(); ++j)
+        if (alphabet[i] == alphabet[j]) { err = "duplicate alphabet symbol"; return false; }
+    for (int k = 0; k < 5; ++k)
+      if (c[k] < 1) { err = "costs must be >= 1"; return false; }
+    for (auto* S : {&P, &N})
+      for (auto& w : *S)
+        for (char ch : w)
+          if (sym_rank(ch) < 0) { err = "symbol not in alphabet"; return false; }
+    for (auto& p : P)
+      for (auto& q : N)
+        if (p == q) { err = "P and N intersect"; return false; }
+    return true;
+  }
+
+  // IC(P u N): every infix of every example, sorted shortlex, deduplicated.
+  void build_ic() {
+    std::vector<std::string> all;
+    for (auto* S : {&P, &N})
+      for (auto& w : *S)
+        for (size_t i = 0; i <= w.size(); ++i)
+          for (size_t j = i; j <= w.size(); ++j) all.push_back(w.substr(i, j - i));
+    std::sort(all.begin(), all.end(),
+              [this](const std::string& a, const std::string& b) { return shortlex_less(a, b); });
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    ic = all;
+    index_of.clear();
+    for (size_t i = 0; i < ic.size(); ++i) index_of[ic[i]] = (int)i;
+    gt.assign(ic.size(), {});
+    for (size_t w = 0; w < ic.size(); ++w)
+      for (size_t k = 0; k <= ic[w].size(); ++k)
+        gt[w].push_back({index_of.at(ic[w].substr(0, k)), index_of.at(ic[w].substr(k))});
+    pos_mask = zero_cs();
+    neg_mask = zero_cs();
+    for (auto& p : P) set_bit(pos_mask, index_of.at(p));
+    for (auto& q : N) set_bit(neg_mask, index_of.at(q));
+  }
+
+  int n() const { return (int)ic.size(); }
+
+  // ---- IPS operations -------------------------------------
+  CS one() const {  // 1(sigma) = [sigma = eps]
+    CS r = zero_cs();
+    set_bit(r, index_of.at(""));
+    return r;
+  }
+  CS op_union(const CS& a, const CS& b) const {  // (r + s)(sigma) = r(sigma) v s(sigma)
+    CS r;
+    for (int k = 0; k < kMaxWords; ++k) r[k] = a[k] | b[k];
+    return r;
+  }
+  // Algorithm 2, lines 5-14: fold over every split in gt[w].
+  CS op_concat(const CS& a, const CS& b) const {
+    CS r = zero_cs();
+    for (int w = 0; w < n(); ++w)
+      for (auto& lr : gt[w])
+        if (test_bit(a, lr.first) && test_bit(b, lr.second)) set_bit(r, w);
+    return r;
+  }
+  // r* = (+)_{n>=0} r^n with r^0 = 1, r^{n+1} = r^n . r:
+  // iterate acc <- 1 + acc . x until it stops changing (finite IC).
+  CS op_star(const CS& x) const {
+    CS acc = one();
+    for (;;) {
+      CS next = op_union(one(), op_concat(acc, x));
+      if (next == acc) return acc;
+      acc = next;
+    }
+  }
+  // r? has the language of eps + r.
+  CS op_question(const CS& x) const { return op_union(one(), x); }
+
+  // L |= (P, N); with allowed error, the number of misclassified
+  // examples is at most the allowed fraction of |P u N|.
+  bool satisfies(const CS& cs) const {
+    if (err_num == 0) {
+      for (int k = 0; k < kMaxWords; ++k) {
+        if ((cs[k] & pos_mask[k]) != pos_mask[k]) return false;
+        if ((cs[k] & neg_mask[k]) != 0) return false;
+      }
+      return true;
+    }
+    long errors = 0;
+    for (auto& p : P) errors += test_bit(cs, index_of.at(p)) ? 0 : 1;
+    for (auto& q : N) errors += test_bit(cs, index_of.at(q)) ? 1 : 0;
+    long total = (long)(P.size() + N.size());
+    return errors * err_den <= err_num * total;
+  }
+
+  // ---- reconstruction ---------------------------------------
+  // Printer: postfix > concat > union; concat and union are associative so
+  // nested same-operator children need no parentheses.
+  enum Prec { PREC_UNION = 0, PREC_CONCAT = 1, PREC_POSTFIX = 2 };
+
+  std::string print_prov(const Prov& p, int* prec_out) const {
+    switch (p.kind) {
+      case K_EMPTY: *prec_out = PREC_POSTFIX; return "empty";
+      case K_EPS: *prec_out = PREC_POSTFIX; return "eps";
+      case K_SYM: *prec_out = PREC_POSTFIX; return std::string(1, alphabet[p.L]);
+      case K_QUESTION:
+      case K_STAR: {
+        int cp;
+        const Prov& child = levels.at(p.L)[p.i].prov;
+        std::string s = print_prov(child, &cp);
+        // a postfix operator binds to one atom: parenthesise anything but a symbol
+        if (child.kind != K_SYM) s = "(" + s + ")";
+        *prec_out = PREC_POSTFIX;
+        return s + (p.kind == K_QUESTION ? "?" : "*");
+      }
+      case K_CONCAT: {
+        int cl, cr;
+        std::string l = print_prov(levels.at(p.L)[p.i].prov, &cl);
+        std::string r = print_prov(levels.at(p.R)[p.j].prov, &cr);
+        if (cl < PREC_CONCAT) l = "(" + l + ")";
+        if (cr < PREC_CONCAT) r = "(" + r + ")";
+        *prec_out = PREC_CONCAT;
+        return l + r;
+      }
+      case K_UNION: {
+        int cl, cr;
+        std::string l = print_prov(levels.at(p.L)[p.i].prov, &cl);
+        std::string r = print_prov(levels.at(p.R)[p.j].prov, &cr);
+        *prec_out = PREC_UNION;
+        return l + "+" + r;
+      }
+    }
+    return "?";
+  }
+  std::string print(const Prov& p) const { int pr; return print_prov(p, &pr); }
+
+  // ---- Algorithm 1 --------------------------------------------
+  uint64_t cand_level = 0;
+  std::vector<Entry>* cur = nullptr;
+  bool found = false;
+  Prov found_prov{};
+  bool oom = false;
+  uint64_t n_entries = 0;
+
+  // One candidate: Alg. 2 lines 15-20.  Every candidate is
+  // counted (reading A9) and tested (reading A11).
+  void emit(const CS& cs, const Prov& prov) {
+    ++cand_level;
+    if (!found) ++candidates;
+    bool sat = satisfies(cs);
+    if (sat && !found) { found = true; found_prov = prov; }
+    if (seen.count(cs)) return;
+    if (max_entries && n_entries >= max_entries) { oom = true; return; }
+    seen.insert(cs);
+    cur->push_back({cs, prov});
+    ++n_entries;
+  }
+
+  bool has_level(int cost) const {
+    auto it = levels.find(cost);
+    return it != levels.end() && !it->second.empty();
+  }
+
+  int solve(int max_cost) {
+    auto t0 = std::chrono::steady_clock::now();
+    levels.clear(); seen.clear(); stats.clear();
+    candidates = 0; cand_complete = 0; found = false; oom = false; n_entries = 0;
+    last_complete_cost = 0; regex.clear(); result_cost = 0;
+    auto done = [&](int st) {
+      status = st;
+      seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      return st;
+    };
+    const int c1 = c[0], c2 = c[1], c3 = c[2], c4 = c[3], c5 = c[4];
+
+    // Alg.1 line 1: the empty regex is the first candidate (reading A9).
+    candidates = 1;
+    {
+      CS z = zero_cs();
+      bool sat_empty = P.empty() || (err_num != 0 && satisfies(z));
+      if (sat_empty) { regex = "empty"; result_cost = c1; return done(0); }
+    }
+    // Alg.1 line 2.
+    if (P.size() == 1 && P[0].empty()) { regex = "eps"; result_cost = c1; return done(0); }
+
+    // Alg.1 line 3: level c1 = CSs of the alphabet symbols, deduplicated and
+    // tested (readings A2, A3).
+    cur = &levels[c1];
+    cand_level = 0;
+    for (size_t a = 0; a < alphabet.size(); ++a) {
+      CS cs = zero_cs();
+      auto it = index_of.find(std::string(1, alphabet[a]));
+      if (it != index_of.end()) set_bit(cs, it->second);
+      emit(cs, Prov{K_SYM, (int)a, 0, 0, 0});
+      if (found) break;
+    }
+    if (found) {
+      regex = print(found_prov); result_cost = c1;
+      stats.push_back({c1, 0, 0, 0, 0, (uint64_t)cur->size(), 0});
+      return done(0);
+    }
+    stats.push_back({c1, 0, 0, 0, 0, (uint64_t)cur->size(), 1});
+    cand_complete = candidates;
+    last_complete_cost = c1;
+
+    // Alg.1 lines 4-9.
+    for (int cost = c1 + 1; cost <= max_cost; ++cost) {
+      std::vector<Entry> fresh;
+      cur = &fresh;
+      LevelStat st{cost, 0, 0, 0, 0, 0, 0};
+      bool stop_emitting = false;
+      auto stop = [&]() { return (found && !complete_final_level) || oom; };
+
+      // buildQuestionMark(c - cost(?))
+      if (has_level(cost - c2)) {
+        cand_level = 0;
+        auto& A = levels[cost - c2];
+        for (size_t i = 0; i < A.size() && !stop(); ++i)
+          emit(op_question(A[i].cs), Prov{K_QUESTION, cost - c2, (long)i, 0, 0});
+        st.cand_q = cand_level;
+      }
+      // buildStar(c - cost(*))
+      if (!stop() && has_level(cost - c3)) {
+        cand_level = 0;
+        auto& A = levels[cost - c3];
+        for (size_t i = 0; i < A.size() && !stop(); ++i)
+          emit(op_star(A[i].cs), Prov{K_STAR, cost - c3, (long)i, 0, 0});
+        st.cand_s = cand_level;
+      }
+      // buildConcat(c - cost(.)) -- Algorithm 2: all (L, R) with L + R = c - c4,
+      // all lCS in level L, all rCS in level R (ordered pairs, reading A7).
+      cand_level = 0;
+      for (int L = c1; L <= cost - c4 - c1 && !stop(); ++L) {
+        int R = cost - c4 - L;
+        if (!has_level(L) || !has_level(R)) continue;
+        auto& A = levels[L];
+        auto& B = levels[R];
+        for (size_t i = 0; i < A.size() && !stop(); ++i)
+          for (size_t j = 0; j < B.size() && !stop(); ++j)
+            emit(op_concat(A[i].cs, B[j].cs), Prov{K_CONCAT, L, (long)i, R, (long)j});
+      }
+      st.cand_c = cand_level;
+      // buildUnion(c - cost(+)) -- unordered pairs L <= R, i < j when L = R (A8).
+      cand_level = 0;
+      for (int L = c1; L <= cost - c5 - L && !stop(); ++L) {
+        int R = cost - c5 - L;
+        if (!has_level(L) || !has_level(R)) continue;
+        auto& A = levels[L];
+        auto& B = levels[R];
+        for (size_t i = 0; i < A.size() && !stop(); ++i)
+          for (size_t j = (L == R ? i + 1 : 0); j < B.size() && !stop(); ++j)
+            emit(op_union(A[i].cs, B[j].cs), Prov{K_UNION, L, (long)i, R, (long)j});
+      }
+      st.cand_u = cand_level;
+      (void)stop_emitting;
+
+      st.unique = fresh.size();
+      bool complete = !oom && (!found || complete_final_level);
+      st.complete = complete ? 1 : 0;
+      if (st.cand_q + st.cand_s + st.cand_c + st.cand_u > 0 || !fresh.empty())
+        stats.push_back(st);
+      levels[cost] = std::move(fresh);  // Alg.1 line 9
+      if (found) {
+        regex = print(found_prov);
+        result_cost = cost;
+        if (complete) { last_complete_cost = cost; }
+        return done(0);
+      }
+      if (oom) return done(3);
+      cand_complete = candidates;
+      last_complete_cost = cost;
+    }
+    return done(2);
+  }
+};
+
+}  // namespace
+
+// ============================ C ABI for ctypes ================================
+extern "C" {
+
+void* orc_create(const char* alphabet, const char* const* P, int nP, const char* const* N,
+                 int nN, const int* costs5, char* errbuf, int errlen) {
+  auto* o = new Oracle();
+  o->alphabet = alphabet;
+  for (int i = 0; i < nP; ++i) o->P.push_back(P[i]);
+  for (int i = 0; i < nN; ++i) o->N.push_back(N[i]);
+  for (int k = 0; k < 5; ++k) o->c[k] = costs5[k];
+  if (!o->validate()) {
+    if (errbuf && errlen > 0) { strncpy(errbuf, o->err.c_str(), errlen - 1); errbuf[errlen - 1] = 0; }
+    delete o;
+    return nullptr;
+  }
+  o->build_ic();
+  if (o->n() > kMaxWords * 64) {
+    if (errbuf && errlen > 0) { strncpy(errbuf, "|IC| > 512", errlen - 1); errbuf[errlen - 1] = 0; }
+    delete o;
+    return nullptr;
+  }
+  return o;
+}
+
+void orc_destroy(void* h) { delete static_cast<Oracle*>(h); }
+
+int orc_n(void* h) { return static_cast<Oracle*>(h)->n(); }
+
+// Copies IC word k into buf (NUL-terminated); returns its length.
+int orc_ic_word(void* h, int k, char* buf, int buflen) {
+  auto* o = static_cast<Oracle*>(h);
+  const std::string& w = o->ic.at(k);
+  int len = (int)w.size();
+  if (buf && buflen > len) { memcpy(buf, w.data(), len); buf[len] = 0; }
+  return len;
+}
+
+// Guide-table row of word w: writes up to cap (l, r) pairs; returns row length.
+int orc_gt_row(void* h, int w, int* pairs, int cap) {
+  auto* o = static_cast<Oracle*>(h);
+  auto& row = o->gt.at(w);
+  for (int k = 0; k < (int)row.size() && k < cap; ++k) {
+    pairs[2 * k] = row[k].first;
+    pairs[2 * k + 1] = row[k].second;
+  }
+  return (int)row.size();
+}
+
+void orc_masks(void* h, uint64_t* pos8, uint64_t* neg8) {
+  auto* o = static_cast<Oracle*>(h);
+  for (int k = 0; k < kMaxWords; ++k) { pos8[k] = o->pos_mask[k]; neg8[k] = o->neg_mask[k]; }
+}
+
+// CS operations on 8-word CSs: op 0 union, 1 concat, 2 star(a), 3 question(a),
+// 4 satisfies(a) (out[0] = 0/1).
+void orc_op(void* h, int op, const uint64_t* a, const uint64_t* b, uint64_t* out) {
+  auto* o = static_cast<Oracle*>(h);
+  CS x, y, r = zero_cs();
+  for (int k = 0; k < kMaxWords; ++k) { x[k] = a[k]; y[k] = b ? b[k] : 0; }
+  switch (op) {
+    case 0: r = o->op_union(x, y); break;
+    case 1: r = o->op_concat(x, y); break;
+    case 2: r = o->op_star(x); break;
+    case 3: r = o->op_question(x); break;
+    case 4: r[0] = o->satisfies(x) ? 1 : 0; break;
+  }
+  for (int k = 0; k < kMaxWords; ++k) out[k] = r[k];
+}
+
+int orc_solve(void* h, int max_cost, long err_num, long err_den, int complete_final_level,
+              unsigned long long max_entries) {
+  auto* o = static_cast<Oracle*>(h);
+  o->err_num = err_num;
+  o->err_den = err_den > 0 ? err_den : 1;
+  o->complete_final_level = complete_final_level != 0;
+  o->max_entries = max_entries;
+  return o->solve(max_cost);
+}
+
+// result: cost, status, candidates (through found), cand_complete, last_complete_cost, seconds
+void orc_result(void* h, long long* out6, double* seconds) {
+  auto* o = static_cast<Oracle*>(h);
+  out6[0] = o->result_cost;
+  out6[1] = o->status;
+  out6[2] = (long long)o->candidates;
+  out6[3] = (long long)o->cand_complete;
+  out6[4] = o->last_complete_cost;
+  out6[5] = (long long)o->n_entries;
+  *seconds = o->seconds;
+}
+
+int orc_regex(void* h, char* buf, int buflen) {
+  auto* o = static_cast<Oracle*>(h);
+  int len = (int)o->regex.size();
+  if (buf && buflen > len) { memcpy(buf, o->regex.data(), len); buf[len] = 0; }
+  return len;
+}
+
+int orc_num_stats(void* h) { return (int)static_cast<Oracle*>(h)->stats.size(); }
+
+// stat k: cost, cand_q, cand_s, cand_c, cand_u, unique, complete
+void orc_stat(void* h, int k, unsigned long long* out7) {
+  auto& s = static_cast<Oracle*>(h)->stats.at(k);
+  out7[0] = s.cost; out7[1] = s.cand_q; out7[2] = s.cand_s; out7[3] = s.cand_c;
+  out7[4] = s.cand_u; out7[5] = s.unique; out7[6] = s.complete;
+}
+
+// Number of cached entries at cost level c (0 if none).
+long orc_level_size(void* h, int cost) {
+  auto* o = static_cast<Oracle*>(h);
+  auto it = o->levels.find(cost);
+  return it == o->levels.end() ? 0 : (long)it->second.size();
+}
+
+// Copies the CSs of level c (8 words each) into out (cap entries).
+long orc_level_cs(void* h, int cost, uint64_t* out, long cap) {
+  auto* o = static_cast<Oracle*>(h);
+  auto it = o->levels.find(cost);
+  if (it == o->levels.end()) return 0;
+  long m = (long)it->second.size();
+  for (long i = 0; i < m && i < cap; ++i)
+    for (int k = 0; k < kMaxWords; ++k) out[i * kMaxWords + k] = it->second[i].cs[k];
+  return m;
+}
+
+// Regex of cached entry i at level c (reconstruction audit).
+int orc_entry_regex(void* h, int cost, long i, char* buf, int buflen) {
+  auto* o = static_cast<Oracle*>(h);
+  std::string s = o->print(o->levels.at(cost).at(i).prov);
+  int len = (int)s.size();
+  if (buf && buflen > len) { memcpy(buf, s.data(), len); buf[len] = 0; }
+  return len;
+}
+
+}  // extern "C"
