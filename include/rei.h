@@ -1,0 +1,163 @@
+/* rei.h -- C ABI of the B200-native Paresy REI hot path (librei_b200.so).
+ *
+ * Precise-and-minimal regular expression inference (REI) by bottom-up,
+ * cost-level-by-cost-level enumeration of characteristic sequences (CS) over
+ * the infix closure IC(P u N), after Valizadeh & Berger, "Search-Based
+ * Regular Expression Inference on a GPU" (arXiv 2305.18575).
+ * Citations: P:n = line n of the paper text; S:n = SPEC.md.
+ *
+ * Conventions for every call:
+ *  - Plain C types and host pointers only; no torch / CUDA types cross the ABI
+ *    (streams and NCCL communicators are passed as opaque `void*`).
+ *  - Every call returns rei_status; no exception crosses the ABI.  After a
+ *    non-OK status, rei_last_error(ctx) describes it (ctx may be NULL for
+ *    rei_init failures: use rei_last_init_error()).
+ *  - A context is NOT thread-safe; use one context per host thread / GPU.
+ *  - All device memory is owned by the context and freed by rei_destroy().
+ *  - Inputs are copied during rei_init; the caller keeps ownership of them.
+ */
+#ifndef REI_B200_H
+#define REI_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; 0/1/2/3 mirror SPEC's exit codes. */
+typedef enum {
+  REI_OK = 0,             /* a minimal precise regex was found                        */
+  REI_EINVAL = 1,         /* invalid input: P cap N != {}, symbol outside Sigma,
+                             cost < 1, duplicate symbol, |IC| > 512, word too long */
+  REI_NOT_FOUND = 2,      /* max_cost exhausted: Alg. 1 "not_found"     */
+  REI_OUT_OF_MEMORY = 3,  /* the language cache / dedup set cannot hold the next level:
+                             the paper's "out-of-memory error"             */
+  REI_ECUDA = 4,          /* a CUDA runtime error (message in rei_last_error)         */
+  REI_ENCCL = 5           /* a collective failed (multi-GPU)                          */
+} rei_status;
+
+/* Cost homomorphism (c1..c5) = (cost(a), cost(?), cost(*), cost(.), cost(+)),
+ * every c_i >= 1.  cost(empty) = cost(eps) = cost(a) = c1. */
+typedef struct {
+  uint32_t sym, opt, star, cat, alt;
+} rei_costs;
+
+/* Option flags. */
+#define REI_FLAG_COMPLETE_FINAL_LEVEL 1u /* finish level c* instead of stopping at the
+                                            first precise CS (for full level counts)  */
+#define REI_FLAG_NO_EARLY_EXIT REI_FLAG_COMPLETE_FINAL_LEVEL
+
+typedef struct {
+  int device;                /* CUDA device ordinal; -1 = the current device             */
+  void* stream;              /* cudaStream_t to run on; NULL = a context-owned stream   */
+  uint64_t mem_budget_bytes; /* device bytes for cache + dedup set; 0 = 80% of free memory */
+  uint32_t err_num, err_den; /* allowed error e = err_num/err_den; 0/x = exact */
+  uint32_t flags;            /* REI_FLAG_*                                                */
+  /* multi-GPU (one context per rank; rei_solve is then collective, S 8(e)) */
+  int world_size;            /* 0 or 1 = single GPU                                       */
+  int rank;
+  const void* nccl_unique_id;/* 128-byte ncclUniqueId, broadcast by the caller (rank 0's) */
+} rei_options;
+
+/* Result of rei_solve.  `regex` is owned by the context and valid until the next
+ * rei_solve or rei_destroy.  Regex syntax is the paper's: union '+', concatenation
+ * by juxtaposition, postfix '?' and '*'; "empty" / "eps" for the trivial answers
+ * (Alg. 1 lines 1-2). */
+typedef struct {
+  const char* regex;
+  uint32_t cost;                /* c*, the minimal cost (valid when status == REI_OK)    */
+  uint32_t last_complete_cost;  /* highest cost level fully enumerated                    */
+  uint64_t candidates;          /* candidates through the last complete level (reading A9)
+                                   plus those evaluated in the final level                 */
+  uint64_t cand_complete;       /* candidates through the last complete level only        */
+  uint64_t unique;              /* CSs in the language cache                              */
+  double seconds;               /* wall time of rei_solve (host clock, device-synchronised) */
+  uint32_t n_ic;                /* |IC(P u N)|, the CS length in bits        */
+  uint32_t cs_words;            /* CS width in 32-bit words (power of two)                */
+} rei_result;
+
+/* Per-cost-level statistics (one entry per non-empty level, ascending cost). */
+typedef struct {
+  uint32_t cost;
+  uint32_t complete;           /* 1 if the level was fully enumerated                   */
+  uint64_t cand_q, cand_s, cand_c, cand_u; /* candidates by outermost constructor (A9)  */
+  uint64_t unique;             /* new unique CSs appended at this level                 */
+  uint64_t evaluated;          /* candidates actually evaluated (== sum of cand_* when complete) */
+  double ms;                   /* device time of the level (CUDA events)                */
+} rei_level_stat;
+
+/* Kernel classes for rei_kernel_stats. */
+typedef enum {
+  REI_K_PRECOMPUTE = 0, REI_K_UNARY = 1, REI_K_CONCAT = 2, REI_K_UNION = 3,
+  REI_K_TRANSPOSE = 4, REI_K_OTHER = 5, REI_K_COUNT = 6
+} rei_kernel_class;
+
+/* rei_init: validate the specification, copy it to the device and run the staged
+ * precompute ON THE DEVICE: IC enumeration in shortlex
+ * order (epsilon = bit 0, LSB first per Alg. 2 line 5/13),
+ * the guide table of proper splits, the P/N masks and the seed CSs.
+ *   alphabet : NUL-terminated string of distinct 1-byte symbols, in Sigma order.
+ *   P, N     : arrays of nP / nN NUL-terminated strings over the alphabet; "" = eps.
+ *   costs    : the cost homomorphism (all >= 1).
+ *   opts     : may be NULL (defaults: current device, own stream, exact, budget 80%).
+ * On success *out receives a new context (free with rei_destroy). */
+rei_status rei_init(void** out, const char* alphabet, const char* const* P, size_t nP,
+                    const char* const* N, size_t nN, rei_costs costs, const rei_options* opts);
+
+/* rei_solve: Algorithm 1 for c = c1 .. max_cost on the device:
+ * per level, ? (x | 1), * (guide-table fixpoint), concatenation (Algorithm 2,
+ * P:1009-1049) and union (bitwise OR) over all operand levels whose costs sum to
+ * the level; every candidate is tested against the P/N masks and
+ * inserted into the dedup set; new CSs are appended to the language
+ * cache with a back-pointer.  Stops at the first level holding a
+ * precise CS and reconstructs its regex.  Returns REI_OK, REI_NOT_FOUND,
+ * REI_OUT_OF_MEMORY (out->last_complete_cost set) or an error. `out` may be NULL. */
+rei_status rei_solve(void* ctx, uint32_t max_cost, rei_result* out);
+
+/* Per-level statistics of the last rei_solve; *n_out = number available. */
+rei_status rei_level_stats(const void* ctx, rei_level_stat* buf, size_t cap, size_t* n_out);
+
+/* Accumulated launches and device milliseconds (CUDA events on the context's stream)
+ * of one kernel class since the last rei_reset_kernel_stats. */
+rei_status rei_kernel_stats(const void* ctx, rei_kernel_class k, uint64_t* launches, double* ms);
+rei_status rei_reset_kernel_stats(void* ctx);
+/* Total kernel launches issued by this context (all classes). */
+uint64_t rei_launch_count(const void* ctx);
+/* Host<->device bytes copied by this context since creation (inputs, level plans,
+ * control lines, results). */
+rei_status rei_transfer_bytes(const void* ctx, uint64_t* h2d, uint64_t* d2h);
+
+const char* rei_last_error(const void* ctx);
+const char* rei_last_init_error(void);
+void rei_destroy(void* ctx);
+
+/* ---- introspection (tests / parity; device data copied back to the host) ---- */
+
+/* |IC| and word k of IC (shortlex index k) copied to buf (NUL-terminated). */
+rei_status rei_ic(const void* ctx, uint32_t k, char* buf, size_t cap, uint32_t* n_ic);
+/* Proper splits (u, v), both non-empty, u v = word w, as pairs of IC
+ * indices written to pairs[2*i], pairs[2*i+1]; *count = number of splits. */
+rei_status rei_splits(const void* ctx, uint32_t w, uint32_t* pairs, size_t cap, uint32_t* count);
+/* P and N masks, cs_words 32-bit words each. */
+rei_status rei_masks(const void* ctx, uint32_t* pos, uint32_t* neg);
+/* The CSs of cost level `cost` of the last solve (cs_words words each, in cache order). */
+rei_status rei_level_cs(const void* ctx, uint32_t cost, uint32_t* out, size_t cap, size_t* count);
+/* Regex reconstructed from cache entry i of level `cost`. */
+rei_status rei_entry_regex(const void* ctx, uint32_t cost, uint64_t i, char* buf, size_t cap);
+/* Apply a CS operation on the device to `count` operand pairs (cs_words words each):
+ * op 0 union, 1 concatenation, 2 star(a), 3 question(a), 4 precise(a) (out word 0 = 0/1). */
+rei_status rei_cs_ops(void* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                      size_t count);
+
+/* ---- multi-GPU host logic (pure functions, usable without a GPU) ---- */
+
+/* Contiguous share of a flattened candidate / work-item space of size `total` for
+ * rank g of G: [*begin, *end) (S 8(e) "Partition"). */
+void rei_partition(uint64_t total, int G, int g, uint64_t* begin, uint64_t* end);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* REI_B200_H */

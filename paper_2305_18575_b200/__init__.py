@@ -1,0 +1,9 @@
+"""B200-native Paresy REI hot path (arXiv 2305.18575).
+
+The search runs in ``librei_b200.so`` (CUDA, sm_100a); ``rei`` is its ctypes
+binding.  ``build`` compiles the library in-tree.  There is no CPU fallback.
+"""
+from .rei import (LevelStat, ReiError, Result, Solver, load_library, partition,  # noqa: F401
+                  solve)
+
+__all__ = ["Solver", "Result", "LevelStat", "ReiError", "solve", "partition", "load_library"]

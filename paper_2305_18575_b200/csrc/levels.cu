@@ -1,0 +1,770 @@
+// levels.cu -- sm_100a level kernels of the REI search (Algorithm 1).
+//
+// Work decomposition:
+//   A *group* = one uniform operand x (warp-uniform) x one slab of 32 consecutive
+//   operands of the other level (one per lane).  A warp evaluates a group of 32
+//   candidates at once:
+//     concat (Alg. 2; IPS product P:637):
+//       lane w computes the bit-slice  acc[w] (bit t = candidate t's bit w)  as
+//         acc[w] = (x[eps] ? T[w] : 0) | (x[w] ? T[eps] : 0)
+//                | OR over proper splits (u, v) of word w with x[u] : T[v]
+//       (x uniform on the left; mirrored when the left side is the sliced one),
+//       where T is the slab in transposed form (T[v] bit t = operand_t[v]) fetched
+//       with warp shuffles; the two epsilon splits of gt(w) are factored out.
+//       A 5-stage shuffle transpose turns the 32 slices into 32 candidate CSs, one
+//       per lane.
+//     union: lane t holds operand_t, candidate = x | operand_t.
+//   Every candidate is then tested for precision and, unless it equals
+//   an operand (guaranteed duplicate), probed in the dedup set;
+//   G groups are batched per lane so each lane keeps G independent probes in
+//   flight.  New CSs are appended with a warp-aggregated atomic.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+
+#include "rei_common.cuh"
+#include "rei_host.h"
+
+namespace cg = cooperative_groups;
+
+namespace rei {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarps = 8;  // warps per CTA of the pair kernels
+// groups per lane batch (independent probes in flight); wide CSs trade MLP for registers
+template <int W> struct Batch { static constexpr int G = (W <= 2) ? 8 : (W == 4 ? 2 : 1); };
+constexpr unsigned long long kEmpty64 = ~0ull;
+constexpr uint32_t kLocked = 0xffffffffu;
+constexpr int kMaxProbe = 1 << 16;
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
+
+// 32x32 bit-matrix transpose across the warp: in lane r, bit c = M[r][c];
+// out lane c, bit r = M[r][c].  Five shuffle stages (block-swap recursion).
+__device__ __forceinline__ uint32_t transpose32(uint32_t x, uint32_t lane) {
+#pragma unroll
+  for (int j = 16; j >= 1; j >>= 1) {
+    const uint32_t m = (j == 16) ? 0x0000FFFFu : (j == 8) ? 0x00FF00FFu
+                     : (j == 4) ? 0x0F0F0F0Fu : (j == 2) ? 0x33333333u : 0x55555555u;
+    const uint32_t y = __shfl_xor_sync(kFull, x, j);
+    x = (lane & j) ? ((x & ~m) | ((y >> j) & m)) : ((x & m) | ((y << j) & ~m));
+  }
+  return x;
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t get_bit(const uint32_t (&x)[W], uint32_t i) {
+  if (W == 1) return (x[0] >> (i & 31)) & 1u;
+  uint32_t word = x[0];
+#pragma unroll
+  for (int q = 1; q < W; ++q) word = ((i >> 5) == (uint32_t)q) ? x[q] : word;
+  return (word >> (i & 31)) & 1u;
+}
+
+template <int W>
+__device__ __forceinline__ bool satisfies(const uint32_t (&cs)[W], const LevelParams& p) {
+  if (p.exact) {
+    uint32_t bad = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) bad |= ((cs[q] & p.pos[q]) ^ p.pos[q]) | (cs[q] & p.neg[q]);
+    return bad == 0;
+  }
+  uint32_t errs = 0;
+#pragma unroll
+  for (int q = 0; q < W; ++q) errs += __popc(p.pos[q] & ~cs[q]) + __popc(p.neg[q] & cs[q]);
+  return errs <= p.max_errors;
+}
+
+template <int W>
+__device__ __forceinline__ bool cs_equal(const uint32_t (&a)[W], const uint32_t (&b)[W]) {
+  uint32_t d = 0;
+#pragma unroll
+  for (int q = 0; q < W; ++q) d |= a[q] ^ b[q];
+  return d == 0;
+}
+
+template <int W>
+__device__ __forceinline__ unsigned long long hash_cs(const uint32_t (&cs)[W]) {
+  unsigned long long h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    h = (h ^ cs[q]) * 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  h *= 0x94D049BB133111EBull;
+  return h ^ (h >> 29);
+}
+
+template <int W>
+__device__ __forceinline__ void load_cs(const uint32_t* __restrict__ arena, uint64_t idx, uint32_t (&x)[W]) {
+  const uint32_t* src = arena + idx * W;
+  if (W == 1) {
+    x[0] = src[0];
+  } else if (W == 2) {
+    const uint2 v = *reinterpret_cast<const uint2*>(src);
+    x[0] = v.x; x[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; q += 4) {
+      const uint4 v = *reinterpret_cast<const uint4*>(src + q);
+      x[q] = v.x; x[q + 1] = v.y; x[q + 2] = v.z; x[q + 3] = v.w;
+    }
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void store_cs(uint32_t* __restrict__ arena, uint64_t idx, const uint32_t (&x)[W]) {
+  uint32_t* dst = arena + idx * W;
+  if (W == 1) {
+    dst[0] = x[0];
+  } else if (W == 2) {
+    *reinterpret_cast<uint2*>(dst) = make_uint2(x[0], x[1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; q += 4)
+      *reinterpret_cast<uint4*>(dst + q) = make_uint4(x[q], x[q + 1], x[q + 2], x[q + 3]);
+  }
+}
+
+// Warp-aggregated append of a new CS + back-pointer to level c.
+template <int W>
+__device__ __forceinline__ void append(const LevelParams& p, const uint32_t (&cs)[W], unsigned long long rank) {
+  cg::coalesced_group g = cg::coalesced_threads();
+  unsigned long long base = 0;
+  if (g.thread_rank() == 0) base = atomicAdd(&p.ctl->count, (unsigned long long)g.size());
+  base = g.shfl(base, 0) + g.thread_rank();
+  const unsigned long long idx = p.out_base + base;
+  if (idx >= p.cap) {
+    p.ctl->overflow = 1;
+    return;
+  }
+  store_cs<W>(p.arena_out, idx, cs);
+  p.bp[idx] = rank;
+}
+
+// ---- dedup: indexed hash set for wide CSs (fingerprint + arena index).
+// Slot = (fp << 32) | idx, 0 = empty, idx == kLocked while the owner writes the CS.
+template <int W>
+__device__ bool insert_indexed(const LevelParams& p, const uint32_t (&cs)[W], unsigned long long rank,
+                               bool do_append, unsigned long long known_idx) {
+  const unsigned long long h = hash_cs<W>(cs);
+  const uint32_t fp = (uint32_t)(h >> 32) | 1u;
+  unsigned long long s = h & p.dedup.mask;
+  for (int probe = 0; probe < kMaxProbe; ++probe) {
+    unsigned long long v = *(volatile unsigned long long*)&p.dedup.table[s];
+    if (v == 0) {
+      const unsigned long long lock = ((unsigned long long)fp << 32) | kLocked;
+      const unsigned long long old = atomicCAS(&p.dedup.table[s], 0ull, lock);
+      if (old == 0) {
+        unsigned long long idx = known_idx;
+        if (do_append) {
+          idx = p.out_base + atomicAdd(&p.ctl->count, 1ull);
+          if (idx >= p.cap || idx >= 0xfffffff0ull) {
+            p.ctl->overflow = 1;
+            atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | 0xfffffffeu);  // dead
+            return false;
+          }
+          store_cs<W>(p.arena_out, idx, cs);
+          p.bp[idx] = rank;
+          __threadfence();
+        }
+        atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | (uint32_t)idx);
+        return true;
+      }
+      v = old;
+    }
+    if ((uint32_t)(v >> 32) == fp) {
+      uint32_t idx = (uint32_t)v;
+      while (idx == kLocked) {
+        __nanosleep(32);
+        idx = (uint32_t)(*(volatile unsigned long long*)&p.dedup.table[s]);
+      }
+      if (idx != 0xfffffffeu) {
+        uint32_t other[W];
+        const volatile uint32_t* src = p.arena_out + (unsigned long long)idx * W;
+#pragma unroll
+        for (int q = 0; q < W; ++q) other[q] = src[q];
+        if (cs_equal<W>(cs, other)) return false;
+      }
+    }
+    s = (s + 1) & p.dedup.mask;
+  }
+  p.ctl->overflow = 1;
+  return false;
+}
+
+// Resolve the insert of a hash64 key whose first slot value is already loaded.
+__device__ __forceinline__ bool insert_hash64(const LevelParams& p, unsigned long long key,
+                                              unsigned long long s, unsigned long long v) {
+  if (key == kEmpty64) return atomicExch(p.dedup.special, 1u) == 0u;
+  for (int probe = 0; probe < kMaxProbe; ++probe) {
+    if (v == key) return false;
+    if (v == kEmpty64) {
+      const unsigned long long old = atomicCAS(&p.dedup.table[s], kEmpty64, key);
+      if (old == kEmpty64) return true;
+      if (old == key) return false;
+    }
+    s = (s + 1) & p.dedup.mask;
+    v = p.dedup.table[s];
+  }
+  p.ctl->overflow = 1;
+  return false;
+}
+
+template <int W>
+__device__ __forceinline__ unsigned long long key64(const uint32_t (&cs)[W]) {
+  return W == 1 ? (unsigned long long)cs[0]
+                : ((unsigned long long)cs[W > 1 ? 1 : 0] << 32) | (unsigned long long)cs[0];
+}
+
+// Batched candidate processing: precision test on every candidate (reading A11),
+// guaranteed duplicates skipped, G probes issued before any is resolved.
+template <int W, int G>
+__device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
+                                              const bool (&skip)[G], const unsigned long long (&rank)[G]) {
+#pragma unroll
+  for (int g = 0; g < G; ++g)
+    if (valid[g] && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, rank[g]);
+
+  if (p.dedup.mode == DEDUP_BITMAP) {
+    uint32_t word[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const bool need = valid[g] && !skip[g];
+      word[g] = need ? p.dedup.bitmap[cs[g][0] >> 5] : kFull;
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const uint32_t bit = 1u << (cs[g][0] & 31);
+      if (!(word[g] & bit)) {
+        const uint32_t old = atomicOr(&p.dedup.bitmap[cs[g][0] >> 5], bit);
+        if (!(old & bit)) append<W>(p, cs[g], rank[g]);
+      }
+    }
+  } else if (p.dedup.mode == DEDUP_HASH64) {
+    unsigned long long slot[G], val[G], key[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const bool need = valid[g] && !skip[g];
+      key[g] = key64<W>(cs[g]);
+      slot[g] = hash_cs<W>(cs[g]) & p.dedup.mask;
+      val[g] = need ? p.dedup.table[slot[g]] : key[g];
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      if (val[g] != key[g] || key[g] == kEmpty64) {
+        const bool need = valid[g] && !skip[g];
+        if (need && insert_hash64(p, key[g], slot[g], val[g])) append<W>(p, cs[g], rank[g]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (valid[g] && !skip[g]) insert_indexed<W>(p, cs[g], rank[g], true, 0);
+  }
+}
+
+// ---- work-item decode (blocks staged in shared memory)
+__device__ __forceinline__ int find_block(const Block* blocks, int nb, unsigned long long item) {
+  int lo = 0, hi = nb - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (blocks[mid].item_off <= item) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ bool found_and_stop(const LevelParams& p) {
+  return p.early_exit && *(volatile unsigned long long*)&p.ctl->found_rank != ~0ull;
+}
+
+// ============================================================================
+// Concatenation kernel.  Dynamic shared memory: split table [maxk][NW], nsplit[NW],
+// blocks[nblocks], and (W > 2) one transposed slab per warp.
+template <int W>
+__global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
+  constexpr int NW = 32 * W;
+  constexpr bool kShfl = (W <= 2);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
+  uint32_t* s_split = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);
+  uint32_t* s_nsplit = s_split + p.maxk * NW;
+  uint32_t* s_T = s_nsplit + NW;  // [kWarps][NW] (W > 2 only)
+
+  for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  for (int i = threadIdx.x; i < (int)(p.maxk * NW); i += blockDim.x)
+    s_split[i] = p.split[(i / NW) * kMaxNW + (i % NW)];
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p.nsplit[i];
+  __syncthreads();
+
+  const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + warp;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+  uint32_t* myT = s_T + warp * (NW + W);
+  uint32_t* myX = myT + NW;  // the uniform operand (W > 2)
+  constexpr int G = Batch<W>::G;
+
+  uint32_t nspl[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) nspl[q] = s_nsplit[q * 32 + lane];
+
+  for (unsigned long long item = gwarp; item < p.total_items; item += nwarps) {
+    if (found_and_stop(p)) break;
+    const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
+    const unsigned long long local = item - blk.item_off;
+    const unsigned long long ut = local / blk.s_tiles, st = local % blk.s_tiles;
+    const bool slice_a = blk.slice_a != 0;
+    const unsigned long long nu = slice_a ? blk.nb : blk.na;
+    const unsigned long long ns = slice_a ? blk.na : blk.nb;
+    const unsigned long long u_base = slice_a ? blk.b_base : blk.a_base;
+    const unsigned long long slab_base = slice_a ? blk.a_slab : blk.b_slab;
+    const unsigned long long u0 = ut * blk.tu, u1 = min(u0 + blk.tu, nu);
+    const unsigned long long nslabs = (ns + 31) / 32;
+    const unsigned long long s0 = st * blk.ts, s1 = min(s0 + blk.ts, nslabs);
+    uint32_t evaluated = 0;
+
+    for (unsigned long long s = s0; s < s1; ++s) {
+      // the slab in transposed form
+      uint32_t T[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) T[q] = p.tarena[(slab_base + s) * NW + q * 32 + lane];
+      if (!kShfl) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) myT[q * 32 + lane] = T[q];
+        __syncwarp();
+      }
+      const uint32_t Teps = __shfl_sync(kFull, T[0], 0);
+      const unsigned long long sj = s * 32 + lane;  // this lane's sliced operand
+      const bool lane_ok = sj < ns;
+
+      for (unsigned long long u = u0; u < u1; u += G) {
+        uint32_t cs[G][W];
+        bool valid[G], skip[G];
+        unsigned long long rank[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const unsigned long long ui = u + g;
+          const bool active = ui < u1;
+          uint32_t x[W];
+          if (active) load_cs<W>(p.arena, u_base + ui, x);
+          else {
+#pragma unroll
+            for (int q = 0; q < W; ++q) x[q] = 0;
+          }
+          const uint32_t xeps = x[0] & 1u;
+          if (!kShfl) {
+            __syncwarp();
+            if (lane == 0) {
+#pragma unroll
+              for (int q = 0; q < W; ++q) myX[q] = x[q];
+            }
+            __syncwarp();
+          }
+          uint32_t acc[W];
+#pragma unroll
+          for (int q = 0; q < W; ++q) acc[q] = (xeps ? T[q] : 0u) | (((x[q] >> lane) & 1u) ? Teps : 0u);
+          for (uint32_t k = 0; k < p.maxk; ++k) {
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+              const uint32_t sp = s_split[k * NW + q * 32 + lane];
+              // x uniform on the left: test x[u], fetch T[v]; mirrored for slice_a.
+              const uint32_t ufix = slice_a ? (sp & 0xffffu) : (sp >> 16);
+              const uint32_t vsl = slice_a ? (sp >> 16) : (sp & 0xffffu);
+              uint32_t t;
+              if (kShfl) {
+                const uint32_t t0 = __shfl_sync(kFull, T[0], vsl & 31);
+                if (W == 2) {
+                  const uint32_t t1 = __shfl_sync(kFull, T[W > 1 ? 1 : 0], vsl & 31);
+                  t = (vsl >> 5) ? t1 : t0;
+                } else {
+                  t = t0;
+                }
+              } else {
+                t = myT[vsl & (NW - 1)];
+              }
+              const uint32_t xb = kShfl ? get_bit<W>(x, ufix) : ((myX[(ufix >> 5) & (W - 1)] >> (ufix & 31)) & 1u);
+              if (k < nspl[q] && xb) acc[q] |= t;
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < W; ++q) cs[g][q] = transpose32(acc[q], lane);
+          valid[g] = active && lane_ok;
+          skip[g] = cs_equal<W>(cs[g], x);  // equals a cached operand: old
+          const unsigned long long i = slice_a ? sj : ui;
+          const unsigned long long j = slice_a ? ui : sj;
+          rank[g] = blk.cand_off + i * blk.nb + j;
+          evaluated += valid[g] ? 1u : 0u;
+        }
+        process_batch<W, G>(p, cs, valid, skip, rank);
+      }
+      if (!kShfl) __syncwarp();
+      if (found_and_stop(p)) break;
+    }
+    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
+    if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
+  }
+}
+
+// ============================================================================
+// Union kernel: uniform operand x, lane t holds operand_t of the sliced level.
+template <int W>
+__global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
+  for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+  constexpr int G = Batch<W>::G;
+
+  for (unsigned long long item = gwarp; item < p.total_items; item += nwarps) {
+    if (found_and_stop(p)) break;
+    const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
+    const unsigned long long local = item - blk.item_off;
+    const unsigned long long ut = local / blk.s_tiles, st = local % blk.s_tiles;
+    const bool slice_a = blk.slice_a != 0;  // uniform = B, sliced = A
+    const bool tri = blk.tri != 0;
+    const unsigned long long nu = slice_a ? blk.nb : blk.na;
+    const unsigned long long ns = slice_a ? blk.na : blk.nb;
+    const unsigned long long u_base = slice_a ? blk.b_base : blk.a_base;
+    const unsigned long long s_base = slice_a ? blk.a_base : blk.b_base;
+    const unsigned long long u0 = ut * blk.tu, u1 = min(u0 + blk.tu, nu);
+    const unsigned long long nslabs = (ns + 31) / 32;
+    unsigned long long s0 = st * blk.ts;
+    const unsigned long long s1 = min(s0 + blk.ts, nslabs);
+    if (tri) s0 = max(s0, (u0 + 1) / 32);  // slabs entirely at or below the diagonal hold no j > i
+    uint32_t evaluated = 0;
+
+    for (unsigned long long s = s0; s < s1; ++s) {
+      const unsigned long long sj = s * 32 + lane;
+      const bool lane_ok = sj < ns;
+      uint32_t y[W];
+      if (lane_ok) load_cs<W>(p.arena, s_base + sj, y);
+      else {
+#pragma unroll
+        for (int q = 0; q < W; ++q) y[q] = 0;
+      }
+      for (unsigned long long u = u0; u < u1; u += G) {
+        if (tri && u >= s * 32 + 31) break;  // no j > i left in this slab
+        uint32_t cs[G][W];
+        bool valid[G], skip[G];
+        unsigned long long rank[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const unsigned long long ui = u + g;
+          bool active = ui < u1;
+          uint32_t x[W];
+          if (active) load_cs<W>(p.arena, u_base + ui, x);
+          else {
+#pragma unroll
+            for (int q = 0; q < W; ++q) x[q] = 0;
+          }
+#pragma unroll
+          for (int q = 0; q < W; ++q) cs[g][q] = x[q] | y[q];
+          const unsigned long long i = slice_a ? sj : ui;
+          const unsigned long long j = slice_a ? ui : sj;
+          valid[g] = active && lane_ok && (!tri || j > i);
+          skip[g] = cs_equal<W>(cs[g], x) || cs_equal<W>(cs[g], y);
+          rank[g] = blk.cand_off +
+                    (tri ? i * blk.na - i * (i + 1) / 2 + (j - i - 1) : i * blk.nb + j);
+          evaluated += valid[g] ? 1u : 0u;
+        }
+        process_batch<W, G>(p, cs, valid, skip, rank);
+      }
+      if (found_and_stop(p)) break;
+    }
+    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
+    if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
+  }
+}
+
+// ============================================================================
+// Unary kernel: thread per operand; first n_q are question marks (x | eps),
+// the rest stars: single shortlex pass  s[eps] = 1,
+//   s[w] = x[w] | OR_{proper (u,v) of w} x[u] & s[v]   (v shorter than w: already final),
+// the least fixpoint of s = 1 + x s (r* = (+)_n r^n).
+template <int W>
+__device__ void star_cs(const uint32_t (&x)[W], uint32_t (&s)[W], uint32_t n, const uint32_t* s_split,
+                        const uint32_t* s_nsplit, int NW) {
+#pragma unroll
+  for (int q = 0; q < W; ++q) s[q] = 0;
+  s[0] = 1u;
+  for (uint32_t w = 1; w < n; ++w) {
+    uint32_t b = get_bit<W>(x, w);
+    const uint32_t m = s_nsplit[w];
+    for (uint32_t k = 0; k < m && !b; ++k) {
+      const uint32_t sp = s_split[k * NW + w];
+      b = get_bit<W>(x, sp >> 16) & get_bit<W>(s, sp & 0xffffu);
+    }
+    if (b) {
+#pragma unroll
+      for (int q = 0; q < W; ++q)
+        if ((w >> 5) == (uint32_t)q) s[q] |= 1u << (w & 31);
+    }
+  }
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long n_q, unsigned long long n_s,
+                                               unsigned long long base_q, unsigned long long base_s,
+                                               unsigned long long off_s) {
+  constexpr int NW = 32 * W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_split = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* s_nsplit = s_split + p.maxk * NW;
+  for (int i = threadIdx.x; i < (int)(p.maxk * NW); i += blockDim.x)
+    s_split[i] = p.split[(i / NW) * kMaxNW + (i % NW)];
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p.nsplit[i];
+  __syncthreads();
+  const unsigned long long total = n_q + n_s;
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    uint32_t x[W], cs[1][W];
+    bool valid[1] = {true}, skip[1];
+    unsigned long long rank[1];
+    if (t < n_q) {
+      load_cs<W>(p.arena, base_q + t, x);
+#pragma unroll
+      for (int q = 0; q < W; ++q) cs[0][q] = x[q];
+      cs[0][0] |= 1u;  // x? = eps + x
+      rank[0] = t;
+    } else {
+      load_cs<W>(p.arena, base_s + (t - n_q), x);
+      star_cs<W>(x, cs[0], p.n, s_split, s_nsplit, NW);
+      rank[0] = off_s + (t - n_q);
+    }
+    skip[0] = cs_equal<W>(cs[0], x);
+    process_batch<W, 1>(p, cs, valid, skip, rank);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&p.ctl->evaluated, total);
+}
+
+// Seeds (Alg. 1 line 3): one thread, symbols in Sigma order (deterministic).
+template <int W>
+__global__ void k_seeds(LevelParams p, const uint32_t* seeds, int nsym) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  for (int a = 0; a < nsym; ++a) {
+    uint32_t cs[1][W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) cs[0][q] = seeds[a * kMaxW32 + q];
+    bool valid[1] = {true}, skip[1] = {false};
+    unsigned long long rank[1] = {(unsigned long long)a};
+    process_batch<W, 1>(p, cs, valid, skip, rank);
+    if (*(volatile unsigned long long*)&p.ctl->found_rank != ~0ull) break;
+  }
+  p.ctl->evaluated = 0;
+}
+
+// Level c -> transposed slabs: warp per slab, T[32q + w] bit t = CS_t[32q + w].
+template <int W>
+__global__ void k_transpose(const uint32_t* __restrict__ arena, unsigned long long base, unsigned long long count,
+                            uint32_t* __restrict__ tarena, unsigned long long slab_base) {
+  constexpr int NW = 32 * W;
+  const uint32_t lane = lane_id();
+  const unsigned long long nslabs = (count + 31) / 32;
+  const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long s = gw; s < nslabs; s += nw) {
+    const unsigned long long e = s * 32 + lane;
+    uint32_t x[W];
+    if (e < count) load_cs<W>(arena, base + e, x);
+    else {
+#pragma unroll
+      for (int q = 0; q < W; ++q) x[q] = 0;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) tarena[(slab_base + s) * NW + q * 32 + lane] = transpose32(x[q], lane);
+  }
+}
+
+// Rebuild the dedup set from the first `count` arena entries (after growth).
+template <int W>
+__global__ void k_rehash(LevelParams p, unsigned long long count) {
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    uint32_t x[W];
+    load_cs<W>(p.arena, t, x);
+    if (p.dedup.mode == DEDUP_BITMAP) {
+      atomicOr(&p.dedup.bitmap[x[0] >> 5], 1u << (x[0] & 31));
+    } else if (p.dedup.mode == DEDUP_HASH64) {
+      const unsigned long long key = key64<W>(x);
+      const unsigned long long s = hash_cs<W>(x) & p.dedup.mask;
+      insert_hash64(p, key, s, p.dedup.table[s]);
+    } else {
+      insert_indexed<W>(p, x, 0, false, t);
+    }
+  }
+}
+
+// Device CS operations on explicit operand pairs (tests): thread per pair, direct
+// fold over the full guide table (epsilon splits + proper splits).
+template <int W>
+__global__ void k_ops(LevelParams p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                      unsigned long long count) {
+  constexpr int NW = 32 * W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_split = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* s_nsplit = s_split + p.maxk * NW;
+  for (int i = threadIdx.x; i < (int)(p.maxk * NW); i += blockDim.x)
+    s_split[i] = p.split[(i / NW) * kMaxNW + (i % NW)];
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p.nsplit[i];
+  __syncthreads();
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    uint32_t x[W], y[W], r[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) { x[q] = a[t * W + q]; y[q] = b ? b[t * W + q] : 0u; r[q] = 0; }
+    if (op == 0) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) r[q] = x[q] | y[q];
+    } else if (op == 1) {
+      for (uint32_t w = 0; w < p.n; ++w) {
+        uint32_t bit = (get_bit<W>(x, 0) & get_bit<W>(y, w)) | (get_bit<W>(x, w) & get_bit<W>(y, 0));
+        for (uint32_t k = 0; k < s_nsplit[w]; ++k) {
+          const uint32_t sp = s_split[k * NW + w];
+          bit |= get_bit<W>(x, sp >> 16) & get_bit<W>(y, sp & 0xffffu);
+        }
+        if (bit) {
+#pragma unroll
+          for (int q = 0; q < W; ++q)
+            if ((w >> 5) == (uint32_t)q) r[q] |= 1u << (w & 31);
+        }
+      }
+    } else if (op == 2) {
+      star_cs<W>(x, r, p.n, s_split, s_nsplit, NW);
+    } else if (op == 3) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) r[q] = x[q];
+      r[0] |= 1u;
+    } else {
+      r[0] = satisfies<W>(x, p) ? 1u : 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) out[t * W + q] = r[q];
+  }
+}
+
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  return sms;
+}
+
+template <typename K>
+int grid_for(K kernel, int threads, size_t smem, unsigned long long work_units_per_cta_hint,
+             unsigned long long work) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+  if (occ <= 0) occ = 1;
+  unsigned long long want = (work + work_units_per_cta_hint - 1) / work_units_per_cta_hint;
+  unsigned long long full = (unsigned long long)sm_count() * occ;
+  if (want < 1) want = 1;
+  return (int)std::min<unsigned long long>(want, full);
+}
+
+size_t pair_smem(const LevelParams& p, int W) {
+  const int NW = 32 * W;
+  size_t s = p.nblocks * sizeof(Block) + (size_t)p.maxk * NW * 4 + NW * 4;
+  if (W > 2) s += (size_t)kWarps * (NW + W) * 4;
+  return s;
+}
+
+template <int W>
+int launch_concat_t(const LevelParams& p, cudaStream_t st) {
+  const size_t smem = pair_smem(p, W);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_concat<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_concat<W>, kWarps * 32, smem, kWarps, p.total_items);
+  k_concat<W><<<grid, kWarps * 32, smem, st>>>(p);
+  return 1;
+}
+
+template <int W>
+int launch_union_t(const LevelParams& p, cudaStream_t st) {
+  const size_t smem = p.nblocks * sizeof(Block);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_union<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_union<W>, kWarps * 32, smem, kWarps, p.total_items);
+  k_union<W><<<grid, kWarps * 32, smem, st>>>(p);
+  return 1;
+}
+
+template <int W>
+int launch_unary_t(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
+                   unsigned long long bq, unsigned long long bs, unsigned long long off_s, cudaStream_t st) {
+  const size_t smem = (size_t)p.maxk * 32 * W * 4 + 32 * W * 4;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_unary<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_unary<W>, 256, smem, 256, n_q + n_s);
+  k_unary<W><<<grid, 256, smem, st>>>(p, n_q, n_s, bq, bs, off_s);
+  return 1;
+}
+
+template <int W>
+int launch_ops_t(const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+                 unsigned long long count, cudaStream_t st) {
+  const size_t smem = (size_t)p.maxk * 32 * W * 4 + 32 * W * 4;
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_ops<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_ops<W>, 256, smem, 256, count);
+  k_ops<W><<<grid, 256, smem, st>>>(p, op, a, b, out, count);
+  return 1;
+}
+
+}  // namespace
+
+#define REI_DISPATCH_W(W32, ...)                 \
+  switch (W32) {                                 \
+    case 1: { constexpr int W = 1; __VA_ARGS__; }   \
+    case 2: { constexpr int W = 2; __VA_ARGS__; }   \
+    case 4: { constexpr int W = 4; __VA_ARGS__; }   \
+    case 8: { constexpr int W = 8; __VA_ARGS__; }   \
+    case 16: { constexpr int W = 16; __VA_ARGS__; } \
+    default: return 0;                           \
+  }
+
+int launch_seeds(int W32, const LevelParams& p, const uint32_t* seeds, int nsym, cudaStream_t st) {
+  REI_DISPATCH_W(W32, k_seeds<W><<<1, 32, 0, st>>>(p, seeds, nsym); return 1);
+}
+
+int launch_unary(int W32, const LevelParams& p, uint64_t n_q, uint64_t n_s, uint64_t bq, uint64_t bs,
+                 uint64_t off_s, cudaStream_t st) {
+  REI_DISPATCH_W(W32, return launch_unary_t<W>(p, n_q, n_s, bq, bs, off_s, st));
+}
+
+int launch_concat(int W32, const LevelParams& p, cudaStream_t st) {
+  REI_DISPATCH_W(W32, return launch_concat_t<W>(p, st));
+}
+
+int launch_union(int W32, const LevelParams& p, cudaStream_t st) {
+  REI_DISPATCH_W(W32, return launch_union_t<W>(p, st));
+}
+
+int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t count, uint32_t* tarena,
+                     uint64_t slab_base, cudaStream_t st) {
+  const unsigned long long slabs = (count + 31) / 32;
+  const int grid = (int)std::min<unsigned long long>((slabs + 7) / 8, (unsigned long long)sm_count() * 8);
+  REI_DISPATCH_W(W32, k_transpose<W><<<std::max(grid, 1), 256, 0, st>>>(arena, base, count, tarena, slab_base);
+                 return 1);
+}
+
+int launch_rehash(int W32, const LevelParams& p, uint64_t count, cudaStream_t st) {
+  const int grid = (int)std::min<unsigned long long>((count + 255) / 256, (unsigned long long)sm_count() * 8);
+  REI_DISPATCH_W(W32, k_rehash<W><<<std::max(grid, 1), 256, 0, st>>>(p, count); return 1);
+}
+
+int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+               uint64_t count, cudaStream_t st) {
+  REI_DISPATCH_W(W32, return launch_ops_t<W>(p, op, a, b, out, count, st));
+}
+
+}  // namespace rei

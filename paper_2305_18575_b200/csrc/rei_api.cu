@@ -1,0 +1,955 @@
+// rei_api.cu -- the C ABI (include/rei.h): context, level scheduler, memory, and
+// regex reconstruction of the B200 REI hot path.
+//
+// Host side of Algorithm 1: for each cost level c the host plans the
+// operand blocks -- Q = lvl(c - c2), S = lvl(c - c3), C = lvl(L) x lvl(R) for all
+// L + R = c - c4 (ordered, reading A7), U = lvl(L) x lvl(R) for L <= R, L + R = c - c5
+// (i < j when L = R, reading A8) -- flattens them into one rank space (Q, S, C by L
+// ascending, U by L ascending, row-major; reading A9 counts candidates from it),
+// launches the level kernels (levels.cu) and reads back one 64-byte control line.
+// The language cache, dedup set and transposed slabs never leave the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/rei.h"
+#include "rei_common.cuh"
+#include "rei_host.h"
+
+namespace rei {
+namespace {
+
+std::string g_init_error;
+
+struct PlanBlock {
+  uint32_t kind;
+  int L, R;
+  uint64_t na, nb;
+  uint64_t cand_off, cand_count;
+  bool tri;
+};
+
+struct LevelInfo {
+  int cost = 0;
+  uint64_t begin = 0;   // arena index
+  uint64_t size = 0;
+  uint64_t slab = 0;    // tarena slab index
+  std::vector<PlanBlock> plan;
+  bool seeds = false;
+};
+
+struct EventPair {
+  cudaEvent_t a, b;
+  int cls;
+};
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string alphabet;
+  std::vector<std::vector<uint8_t>> P, N;
+  rei_costs costs{};
+  uint32_t err_num = 0, err_den = 1;
+  uint32_t flags = 0;
+  uint64_t budget = 0;
+
+  DeviceTables tab;
+  int W32 = 1;
+  int mode = DEDUP_BITMAP;
+
+  // device buffers
+  uint32_t* arena = nullptr;
+  unsigned long long* bp = nullptr;
+  uint32_t* tarena = nullptr;
+  uint64_t cap = 0;        // entries
+  uint64_t slab_cap = 0;   // slabs
+  uint32_t* bitmap = nullptr;
+  uint64_t bitmap_words = 0;
+  unsigned long long* table = nullptr;
+  uint64_t slots = 0;
+  unsigned int* special = nullptr;
+  LevelCtl* ctl = nullptr;
+  LevelCtl* h_ctl = nullptr;  // pinned
+  Block* d_blocks = nullptr;  // [2][kMaxBlocks]
+  Block* h_blocks = nullptr;  // pinned
+  static constexpr int kMaxBlocks = 4096;
+
+  // search state
+  std::map<int, LevelInfo> levels;
+  uint64_t arena_used = 0, slabs_used = 0;
+  std::vector<rei_level_stat> stats;
+  std::string regex;
+  std::string err;
+  rei_result result{};
+
+  // profiling
+  uint64_t h2d_bytes = 0, d2h_bytes = 0;
+  uint64_t launches = 0;
+  uint64_t k_launches[REI_K_COUNT] = {0};
+  double k_ms[REI_K_COUNT] = {0};
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  std::vector<EventPair> pending;
+
+  ~Ctx() {
+    if (stream) cudaStreamSynchronize(stream);
+    cudaFree(arena); cudaFree(bp); cudaFree(tarena); cudaFree(bitmap); cudaFree(table);
+    cudaFree(special); cudaFree(ctl); cudaFree(d_blocks);
+    cudaFree(tab.split); cudaFree(tab.nsplit); cudaFree(tab.word_len); cudaFree(tab.seeds);
+    if (h_ctl) cudaFreeHost(h_ctl);
+    if (h_blocks) cudaFreeHost(h_blocks);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (own_stream && stream) cudaStreamDestroy(stream);
+  }
+
+  cudaEvent_t next_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
+  void begin_kernel(int cls, EventPair& ep) {
+    ep.a = next_event();
+    ep.b = next_event();
+    ep.cls = cls;
+    cudaEventRecord(ep.a, stream);
+  }
+  void end_kernel(EventPair& ep, int n) {
+    cudaEventRecord(ep.b, stream);
+    launches += n;
+    k_launches[ep.cls] += n;
+    pending.push_back(ep);
+  }
+  // after a stream sync: fold the pending event pairs into the per-class totals
+  void collect_events(double* level_ms) {
+    double tot = 0;
+    for (auto& ep : pending) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ep.a, ep.b);
+      k_ms[ep.cls] += ms;
+      tot += ms;
+    }
+    pending.clear();
+    ev_next = 0;
+    if (level_ms) *level_ms = tot;
+  }
+};
+
+#define CUDA_OK(c, x)                                                        \
+  do {                                                                       \
+    cudaError_t e__ = (x);                                                   \
+    if (e__ != cudaSuccess) {                                                \
+      (c)->err = std::string(#x ": ") + cudaGetErrorString(e__);             \
+      return REI_ECUDA;                                                      \
+    }                                                                        \
+  } while (0)
+
+int next_pow2_words(int n) {
+  int w = (n + 31) / 32;
+  int p = 1;
+  while (p < w) p <<= 1;
+  return p;
+}
+
+uint64_t bytes_per_entry(const Ctx* c) {
+  // CS + back-pointer + transposed copy (+ hash slots at load <= 1/2)
+  uint64_t b = 4ull * c->W32 + 8 + 4ull * c->W32;
+  if (c->mode != DEDUP_BITMAP) b += 16;
+  return b;
+}
+
+// (Re)allocate arena, bp, tarena for `cap` entries, preserving the first `keep` entries.
+rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_slabs) {
+  const uint64_t new_slab_cap = new_cap / 32 + 4096;
+  uint32_t* a = nullptr;
+  unsigned long long* b = nullptr;
+  uint32_t* t = nullptr;
+  CUDA_OK(c, cudaMalloc(&a, new_cap * 4ull * c->W32));
+  CUDA_OK(c, cudaMalloc(&b, new_cap * 8ull));
+  CUDA_OK(c, cudaMalloc(&t, new_slab_cap * 32ull * c->W32 * 4ull));
+  if (keep) {
+    CUDA_OK(c, cudaMemcpyAsync(a, c->arena, keep * 4ull * c->W32, cudaMemcpyDeviceToDevice, c->stream));
+    CUDA_OK(c, cudaMemcpyAsync(b, c->bp, keep * 8ull, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  if (keep_slabs)
+    CUDA_OK(c, cudaMemcpyAsync(t, c->tarena, keep_slabs * 32ull * c->W32 * 4ull, cudaMemcpyDeviceToDevice,
+                               c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  cudaFree(c->arena); cudaFree(c->bp); cudaFree(c->tarena);
+  c->arena = a; c->bp = b; c->tarena = t;
+  c->cap = new_cap;
+  c->slab_cap = new_slab_cap;
+  if (c->mode != DEDUP_BITMAP) {
+    uint64_t want = 1;
+    while (want < 2 * new_cap) want <<= 1;
+    if (want != c->slots) {
+      cudaFree(c->table);
+      c->table = nullptr;
+      CUDA_OK(c, cudaMalloc(&c->table, want * 8ull));
+      c->slots = want;
+    }
+  }
+  return REI_OK;
+}
+
+void fill_params(Ctx* c, LevelParams& p) {
+  memset(&p, 0, sizeof(p));
+  p.arena = c->arena;
+  p.arena_out = c->arena;
+  p.tarena = c->tarena;
+  p.bp = c->bp;
+  p.n = (uint32_t)c->tab.n;
+  p.maxk = (uint32_t)c->tab.maxk;
+  p.exact = c->err_num == 0 ? 1 : 0;
+  const uint64_t total = c->P.size() + c->N.size();
+  p.max_errors = c->err_num ? (uint32_t)((uint64_t)c->err_num * total / c->err_den) : 0;
+  p.early_exit = (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL) ? 0 : 1;
+  p.cap = c->cap;
+  p.split = c->tab.split;
+  p.nsplit = c->tab.nsplit;
+  p.ctl = c->ctl;
+  p.dedup.mode = c->mode;
+  p.dedup.bitmap = c->bitmap;
+  p.dedup.table = c->table;
+  p.dedup.mask = c->slots ? c->slots - 1 : 0;
+  p.dedup.special = c->special;
+  for (int q = 0; q < kMaxW32; ++q) { p.pos[q] = c->tab.pos[q]; p.neg[q] = c->tab.neg[q]; }
+}
+
+rei_status clear_dedup(Ctx* c) {
+  if (c->mode == DEDUP_BITMAP) {
+    CUDA_OK(c, cudaMemsetAsync(c->bitmap, 0, c->bitmap_words * 4, c->stream));
+  } else {
+    CUDA_OK(c, cudaMemsetAsync(c->table, c->mode == DEDUP_HASH64 ? 0xff : 0x00, c->slots * 8, c->stream));
+    CUDA_OK(c, cudaMemsetAsync(c->special, 0, sizeof(unsigned int), c->stream));
+  }
+  return REI_OK;
+}
+
+rei_status reset_ctl(Ctx* c) {
+  LevelCtl z;
+  memset(&z, 0, sizeof(z));
+  z.found_rank = ~0ull;
+  *c->h_ctl = z;
+  CUDA_OK(c, cudaMemcpyAsync(c->ctl, c->h_ctl, sizeof(LevelCtl), cudaMemcpyHostToDevice, c->stream));
+  c->h2d_bytes += sizeof(LevelCtl);
+  return REI_OK;
+}
+
+rei_status read_ctl(Ctx* c) {
+  CUDA_OK(c, cudaMemcpyAsync(c->h_ctl, c->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->d2h_bytes += sizeof(LevelCtl);
+  return REI_OK;
+}
+
+uint64_t level_size(const Ctx* c, int cost) {
+  auto it = c->levels.find(cost);
+  return it == c->levels.end() ? 0 : it->second.size;
+}
+
+// Decode a rank of level `cost` into (kind, L, i, R, j) (inverse of the flattening).
+struct Node {
+  uint32_t kind;  // 0..3 = Q S C U, 4 = symbol
+  int L, R;
+  uint64_t i, j;
+};
+
+Node decode_rank(const Ctx* c, int cost, uint64_t rank) {
+  const LevelInfo& lv = c->levels.at(cost);
+  Node nd{};
+  if (lv.seeds) { nd.kind = 4; nd.i = rank; return nd; }
+  for (const PlanBlock& b : lv.plan) {
+    if (rank < b.cand_off || rank >= b.cand_off + b.cand_count) continue;
+    const uint64_t t = rank - b.cand_off;
+    nd.kind = b.kind;
+    nd.L = b.L;
+    nd.R = b.R;
+    if (b.kind == BK_Q || b.kind == BK_S) { nd.i = t; return nd; }
+    if (!b.tri) { nd.i = t / b.nb; nd.j = t % b.nb; return nd; }
+    // triangular: start(i) = i*m - i(i+1)/2; largest i with start(i) <= t
+    const uint64_t m = b.na;
+    uint64_t lo = 0, hi = m - 1;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi + 1) / 2;
+      const uint64_t start = mid * m - mid * (mid + 1) / 2;
+      if (start <= t) lo = mid; else hi = mid - 1;
+    }
+    nd.i = lo;
+    nd.j = t - (lo * m - lo * (lo + 1) / 2) + lo + 1;
+    return nd;
+  }
+  nd.kind = 99;
+  return nd;
+}
+
+// Printer (paper syntax): postfix > concatenation > union; a postfix operator wraps
+// any operand that is not a single symbol; concatenation wraps union operands.
+enum { PR_UNION = 0, PR_CAT = 1, PR_ATOM = 2 };
+
+bool rebuild(Ctx* c, int cost, uint64_t rank, std::string& out, int& prec, int depth);
+
+bool rebuild_entry(Ctx* c, int cost, uint64_t idx, std::string& out, int& prec, int depth) {
+  const LevelInfo& lv = c->levels.at(cost);
+  unsigned long long r = 0;
+  if (cudaMemcpy(&r, c->bp + lv.begin + idx, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+  c->d2h_bytes += 8;
+  return rebuild(c, cost, r, out, prec, depth + 1);
+}
+
+bool rebuild(Ctx* c, int cost, uint64_t rank, std::string& out, int& prec, int depth) {
+  if (depth > 100000) return false;
+  Node nd = decode_rank(c, cost, rank);
+  const rei_costs& k = c->costs;
+  switch (nd.kind) {
+    case 4:
+      out = std::string(1, c->alphabet[nd.i]);
+      prec = PR_ATOM;
+      return true;
+    case BK_Q:
+    case BK_S: {
+      const int L = (nd.kind == BK_Q) ? cost - (int)k.opt : cost - (int)k.star;
+      std::string s;
+      int ps;
+      if (!rebuild_entry(c, L, nd.i, s, ps, depth)) return false;
+      if (!(ps == PR_ATOM && s.size() == 1)) s = "(" + s + ")";
+      out = s + (nd.kind == BK_Q ? "?" : "*");
+      prec = PR_ATOM;
+      return true;
+    }
+    case BK_C:
+    case BK_U: {
+      std::string l, r;
+      int pl, pr;
+      if (!rebuild_entry(c, nd.L, nd.i, l, pl, depth)) return false;
+      if (!rebuild_entry(c, nd.R, nd.j, r, pr, depth)) return false;
+      if (nd.kind == BK_C) {
+        if (pl == PR_UNION) l = "(" + l + ")";
+        if (pr == PR_UNION) r = "(" + r + ")";
+        out = l + r;
+        prec = PR_CAT;
+      } else {
+        out = l + "+" + r;
+        prec = PR_UNION;
+      }
+      return true;
+    }
+  }
+  return false;
+}
+
+// Build the level plan for cost c from the sizes of lower levels.
+void plan_level(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std::vector<Block>& uni,
+                uint64_t& nq, uint64_t& ns, uint64_t& ncat, uint64_t& nuni) {
+  const rei_costs& k = c->costs;
+  const int c1 = (int)k.sym;
+  uint64_t off = 0;
+  lv.plan.clear();
+  cat.clear();
+  uni.clear();
+  nq = level_size(c, cost - (int)k.opt);
+  if (cost - (int)k.opt < c1) nq = 0;
+  if (nq) { lv.plan.push_back({BK_Q, cost - (int)k.opt, 0, nq, 0, off, nq, false}); off += nq; }
+  ns = level_size(c, cost - (int)k.star);
+  if (cost - (int)k.star < c1) ns = 0;
+  if (ns) { lv.plan.push_back({BK_S, cost - (int)k.star, 0, ns, 0, off, ns, false}); off += ns; }
+  ncat = 0;
+  const uint64_t target = 8192;  // candidates per work item
+  uint64_t item_off = 0;
+  for (int L = c1; L <= cost - (int)k.cat - c1; ++L) {
+    const int R = cost - (int)k.cat - L;
+    const uint64_t na = level_size(c, L), nb = level_size(c, R);
+    if (!na || !nb) continue;
+    PlanBlock pb{BK_C, L, R, na, nb, off, na * nb, false};
+    lv.plan.push_back(pb);
+    Block b{};
+    b.kind = BK_C;
+    b.slice_a = (na > nb) ? 1 : 0;  // slice the larger side, the smaller is uniform
+    const LevelInfo& A = c->levels.at(L);
+    const LevelInfo& B = c->levels.at(R);
+    b.a_base = A.begin; b.b_base = B.begin; b.a_slab = A.slab; b.b_slab = B.slab;
+    b.na = na; b.nb = nb;
+    b.cand_off = off; b.cand_count = na * nb;
+    const uint64_t nu = b.slice_a ? nb : na, nsl = b.slice_a ? na : nb;
+    const uint64_t slabs = (nsl + 31) / 32;
+    b.tu = std::min<uint64_t>(64, nu);
+    b.ts = std::max<uint64_t>(1, std::min<uint64_t>(slabs, target / (32 * b.tu)));
+    b.u_tiles = (nu + b.tu - 1) / b.tu;
+    b.s_tiles = (slabs + b.ts - 1) / b.ts;
+    b.item_off = item_off;
+    item_off += b.u_tiles * b.s_tiles;
+    cat.push_back(b);
+    off += na * nb;
+    ncat += na * nb;
+  }
+  nuni = 0;
+  item_off = 0;
+  for (int L = c1; L <= cost - (int)k.alt - L; ++L) {
+    const int R = cost - (int)k.alt - L;
+    const uint64_t na = level_size(c, L), nb = level_size(c, R);
+    if (!na || !nb) continue;
+    const bool tri = (L == R);
+    const uint64_t cnt = tri ? na * (na - 1) / 2 : na * nb;
+    if (!cnt) continue;
+    lv.plan.push_back({BK_U, L, R, na, nb, off, cnt, tri});
+    Block b{};
+    b.kind = BK_U;
+    b.tri = tri ? 1 : 0;
+    b.slice_a = (!tri && na > nb) ? 1 : 0;
+    const LevelInfo& A = c->levels.at(L);
+    const LevelInfo& B = c->levels.at(R);
+    b.a_base = A.begin; b.b_base = B.begin; b.a_slab = A.slab; b.b_slab = B.slab;
+    b.na = na; b.nb = nb;
+    b.cand_off = off; b.cand_count = cnt;
+    const uint64_t nu = b.slice_a ? nb : na, nsl = b.slice_a ? na : nb;
+    const uint64_t slabs = (nsl + 31) / 32;
+    b.tu = std::min<uint64_t>(64, nu);
+    b.ts = std::max<uint64_t>(1, std::min<uint64_t>(slabs, target / (32 * b.tu)));
+    b.u_tiles = (nu + b.tu - 1) / b.tu;
+    b.s_tiles = (slabs + b.ts - 1) / b.ts;
+    b.item_off = item_off;
+    item_off += b.u_tiles * b.s_tiles;
+    uni.push_back(b);
+    off += cnt;
+    nuni += cnt;
+  }
+}
+
+uint64_t items_of(const std::vector<Block>& v) {
+  if (v.empty()) return 0;
+  return v.back().item_off + v.back().u_tiles * v.back().s_tiles;
+}
+
+rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
+  rei_status s = clear_dedup(c);
+  if (s != REI_OK) return s;
+  if (!entries) return REI_OK;
+  LevelParams p;
+  fill_params(c, p);
+  EventPair ep;
+  c->begin_kernel(REI_K_OTHER, ep);
+  int n = launch_rehash(c->W32, p, entries, c->stream);
+  c->end_kernel(ep, n);
+  CUDA_OK(c, cudaGetLastError());
+  return REI_OK;
+}
+
+rei_status grow(Ctx* c, uint64_t need_entries) {
+  const uint64_t max_cap = c->budget / bytes_per_entry(c);
+  if (c->cap >= max_cap) return REI_OUT_OF_MEMORY;
+  uint64_t nc = std::max<uint64_t>(c->cap * 4, need_entries);
+  if (c->mode == DEDUP_BITMAP) nc = std::min<uint64_t>(nc, (1ull << c->tab.n) + 64);
+  nc = std::min(nc, max_cap);
+  if (nc <= c->cap) return REI_OUT_OF_MEMORY;
+  rei_status s = alloc_arena(c, nc, c->arena_used, c->slabs_used);
+  if (s != REI_OK) return s;
+  return rebuild_dedup(c, c->arena_used);
+}
+
+rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
+  std::string rx;
+  int pr;
+  if (!rebuild(c, cost, rank, rx, pr, 0)) {
+    c->err = "regex reconstruction failed";
+    return REI_ECUDA;
+  }
+  c->regex = rx;
+  c->result.cost = (uint32_t)cost;
+  return REI_OK;
+}
+
+rei_status solve_impl(Ctx* c, uint32_t max_cost) {
+  const rei_costs& k = c->costs;
+  const int c1 = (int)k.sym;
+  c->levels.clear();
+  c->stats.clear();
+  c->regex.clear();
+  c->arena_used = 0;
+  c->slabs_used = 0;
+  memset(&c->result, 0, sizeof(c->result));
+  c->result.n_ic = (uint32_t)c->tab.n;
+  c->result.cs_words = (uint32_t)c->W32;
+  uint64_t cand = 1;  // Alg. 1 line 1: the empty regex is the first candidate (A9)
+
+  const uint64_t total_ex = c->P.size() + c->N.size();
+  const bool empty_ok = c->P.empty() ||
+                        (c->err_num && (uint64_t)c->P.size() * c->err_den <= (uint64_t)c->err_num * total_ex);
+  if (empty_ok) {
+    c->regex = "empty";
+    c->result.cost = k.sym;
+    c->result.candidates = cand;
+    return REI_OK;
+  }
+  if (c->P.size() == 1 && c->P[0].empty()) {  // Alg. 1 line 2
+    c->regex = "eps";
+    c->result.cost = k.sym;
+    c->result.candidates = cand;
+    return REI_OK;
+  }
+  rei_status s = clear_dedup(c);
+  if (s != REI_OK) return s;
+
+  // ---- level c1: the alphabet symbols (Alg. 1 line 3)
+  {
+    LevelInfo lv;
+    lv.cost = c1;
+    lv.begin = 0;
+    lv.seeds = true;
+    LevelParams p;
+    fill_params(c, p);
+    p.out_base = 0;
+    if ((s = reset_ctl(c)) != REI_OK) return s;
+    EventPair ep;
+    c->begin_kernel(REI_K_OTHER, ep);
+    int n = launch_seeds(c->W32, p, c->tab.seeds, (int)c->alphabet.size(), c->stream);
+    c->end_kernel(ep, n);
+    CUDA_OK(c, cudaGetLastError());
+    if ((s = read_ctl(c)) != REI_OK) return s;
+    double ms;
+    c->collect_events(&ms);
+    lv.size = c->h_ctl->count;
+    cand += c->alphabet.size();
+    c->levels[c1] = lv;
+    c->arena_used = lv.size;
+    rei_level_stat st{};
+    st.cost = c1;
+    st.unique = lv.size;
+    st.ms = ms;
+    if (c->h_ctl->found_rank != ~0ull) {
+      const uint64_t r = c->h_ctl->found_rank;
+      cand = 1 + r + 1;
+      st.complete = 0;
+      c->stats.push_back(st);
+      c->result.candidates = cand;
+      return finish_found(c, c1, r);
+    }
+    st.complete = 1;
+    c->stats.push_back(st);
+    c->levels[c1].slab = 0;
+    EventPair et;
+    c->begin_kernel(REI_K_TRANSPOSE, et);
+    n = launch_transpose(c->W32, c->arena, 0, lv.size, c->tarena, 0, c->stream);
+    c->end_kernel(et, n);
+    c->slabs_used = (lv.size + 31) / 32;
+    c->result.last_complete_cost = c1;
+    c->result.cand_complete = cand;
+  }
+
+  std::vector<Block> cat, uni;
+  for (int cost = c1 + 1; cost <= (int)max_cost; ++cost) {
+    LevelInfo lv;
+    lv.cost = cost;
+    uint64_t nq, ns, ncat, nuni;
+    plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);
+    if (lv.plan.empty()) continue;
+    if ((int)(cat.size() + uni.size()) > Ctx::kMaxBlocks) {
+      c->err = "too many operand blocks in one level";
+      return REI_EINVAL;
+    }
+    lv.begin = c->arena_used;
+    lv.slab = c->slabs_used;
+    rei_level_stat st{};
+    st.cost = (uint32_t)cost;
+    st.cand_q = nq; st.cand_s = ns; st.cand_c = ncat; st.cand_u = nuni;
+    double level_ms = 0;
+    for (int attempt = 0;; ++attempt) {
+      LevelParams p;
+      fill_params(c, p);
+      p.out_base = lv.begin;
+      if ((s = reset_ctl(c)) != REI_OK) return s;
+      // operand blocks -> device (one small H2D per level)
+      std::copy(cat.begin(), cat.end(), c->h_blocks);
+      std::copy(uni.begin(), uni.end(), c->h_blocks + Ctx::kMaxBlocks);
+      if (!cat.empty())
+        CUDA_OK(c, cudaMemcpyAsync(c->d_blocks, c->h_blocks, cat.size() * sizeof(Block), cudaMemcpyHostToDevice,
+                                   c->stream));
+      if (!uni.empty())
+        CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + Ctx::kMaxBlocks, c->h_blocks + Ctx::kMaxBlocks,
+                                   uni.size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
+      c->h2d_bytes += (cat.size() + uni.size()) * sizeof(Block);
+      if (nq + ns) {
+        const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
+        const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
+        EventPair ep;
+        c->begin_kernel(REI_K_UNARY, ep);
+        int n = launch_unary(c->W32, p, nq, ns, bq, bs, nq, c->stream);
+        c->end_kernel(ep, n);
+      }
+      if (!cat.empty()) {
+        LevelParams pc = p;
+        pc.blocks = c->d_blocks;
+        pc.nblocks = (uint32_t)cat.size();
+        pc.total_items = items_of(cat);
+        EventPair ep;
+        c->begin_kernel(REI_K_CONCAT, ep);
+        int n = launch_concat(c->W32, pc, c->stream);
+        c->end_kernel(ep, n);
+      }
+      if (!uni.empty()) {
+        LevelParams pu = p;
+        pu.blocks = c->d_blocks + Ctx::kMaxBlocks;
+        pu.nblocks = (uint32_t)uni.size();
+        pu.total_items = items_of(uni);
+        EventPair ep;
+        c->begin_kernel(REI_K_UNION, ep);
+        int n = launch_union(c->W32, pu, c->stream);
+        c->end_kernel(ep, n);
+      }
+      CUDA_OK(c, cudaGetLastError());
+      if ((s = read_ctl(c)) != REI_OK) return s;
+      double ms;
+      c->collect_events(&ms);
+      level_ms += ms;
+      if (!c->h_ctl->overflow) break;
+      // capacity exceeded: grow the cache / dedup set and redo the level
+      const uint64_t need = lv.begin + c->h_ctl->count + 1;
+      s = grow(c, need);
+      if (s != REI_OK) {
+        c->result.candidates = c->result.cand_complete;
+        return s;
+      }
+    }
+    lv.size = c->h_ctl->count;
+    c->arena_used = lv.begin + lv.size;
+    st.unique = lv.size;
+    st.ms = level_ms;
+    const bool found = c->h_ctl->found_rank != ~0ull;
+    const bool complete = !found || (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
+    st.complete = complete ? 1 : 0;
+    st.evaluated = complete ? (nq + ns + ncat + nuni) : c->h_ctl->evaluated;
+    c->levels[cost] = lv;
+    c->stats.push_back(st);
+    if (found) {
+      c->result.candidates = cand + st.evaluated;
+      if (complete) {
+        c->result.last_complete_cost = (uint32_t)cost;
+        c->result.cand_complete = cand + st.evaluated;
+      }
+      return finish_found(c, cost, c->h_ctl->found_rank);
+    }
+    cand += nq + ns + ncat + nuni;
+    c->result.cand_complete = cand;
+    c->result.candidates = cand;
+    c->result.last_complete_cost = (uint32_t)cost;
+    // transposed copy of level c (the sliced-operand layout for later levels)
+    if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
+      if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
+    }
+    EventPair et;
+    c->begin_kernel(REI_K_TRANSPOSE, et);
+    int n = launch_transpose(c->W32, c->arena, lv.begin, lv.size, c->tarena, lv.slab, c->stream);
+    c->end_kernel(et, n);
+    c->slabs_used += (lv.size + 31) / 32;
+  }
+  return REI_NOT_FOUND;
+}
+
+}  // namespace
+}  // namespace rei
+
+using rei::Ctx;
+
+extern "C" {
+
+rei_status rei_init(void** out, const char* alphabet, const char* const* P, size_t nP, const char* const* N,
+                    size_t nN, rei_costs costs, const rei_options* opts) {
+  using namespace rei;
+  g_init_error.clear();
+  if (!out || !alphabet) { g_init_error = "null argument"; return REI_EINVAL; }
+  *out = nullptr;
+  auto c = std::make_unique<Ctx>();
+  c->alphabet = alphabet;
+  const size_t k = c->alphabet.size();
+  if (k == 0 || k > 255) { g_init_error = "alphabet must have 1..255 symbols"; return REI_EINVAL; }
+  int rank_of[256];
+  for (int i = 0; i < 256; ++i) rank_of[i] = -1;
+  for (size_t i = 0; i < k; ++i) {
+    const unsigned char ch = (unsigned char)c->alphabet[i];
+    if (rank_of[ch] >= 0) { g_init_error = "duplicate alphabet symbol"; return REI_EINVAL; }
+    rank_of[ch] = (int)i;
+  }
+  if (!costs.sym || !costs.opt || !costs.star || !costs.cat || !costs.alt) {
+    g_init_error = "every constructor cost must be >= 1 (P:483)";
+    return REI_EINVAL;
+  }
+  c->costs = costs;
+  // longest word whose shortlex key (value < 2^58) is exact
+  int max_len = 0;
+  {
+    long double v = 1;
+    while (v * k < (long double)(1ull << 58) && max_len < 63) { v *= k; ++max_len; }
+  }
+  auto conv = [&](const char* const* S, size_t m, std::vector<std::vector<uint8_t>>& dst) -> bool {
+    for (size_t i = 0; i < m; ++i) {
+      if (!S[i]) { g_init_error = "null example string"; return false; }
+      std::vector<uint8_t> w;
+      for (const char* q = S[i]; *q; ++q) {
+        const int r = rank_of[(unsigned char)*q];
+        if (r < 0) { g_init_error = "example symbol not in the alphabet"; return false; }
+        w.push_back((uint8_t)r);
+      }
+      if ((int)w.size() > max_len) { g_init_error = "example too long for the 58-bit shortlex key"; return false; }
+      dst.push_back(w);
+    }
+    return true;
+  };
+  if (!conv(P, nP, c->P) || !conv(N, nN, c->N)) return REI_EINVAL;
+  for (auto& p : c->P)
+    for (auto& q : c->N)
+      if (p == q) { g_init_error = "P and N intersect (P:472-477)"; return REI_EINVAL; }
+  // dedup of repeated examples within P or N (sets)
+  auto dedup_set = [](std::vector<std::vector<uint8_t>>& v) {
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+  };
+  dedup_set(c->P);
+  dedup_set(c->N);
+  if (opts) {
+    c->err_num = opts->err_num;
+    c->err_den = opts->err_den ? opts->err_den : 1;
+    c->flags = opts->flags;
+    c->budget = opts->mem_budget_bytes;
+    if (opts->world_size > 1) { g_init_error = "multi-GPU contexts: use rei_init_mgpu"; return REI_EINVAL; }
+  }
+  if (opts && opts->device >= 0) {
+    if (cudaSetDevice(opts->device) != cudaSuccess) { g_init_error = "cudaSetDevice failed"; return REI_ECUDA; }
+    c->device = opts->device;
+  } else {
+    cudaGetDevice(&c->device);
+  }
+  if (opts && opts->stream) {
+    c->stream = (cudaStream_t)opts->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      g_init_error = "no CUDA device / stream creation failed";
+      return REI_ECUDA;
+    }
+    c->own_stream = true;
+  }
+  auto fail = [&](const std::string& m) { g_init_error = m; return REI_ECUDA; };
+  if (cudaMalloc(&c->tab.split, sizeof(uint32_t) * kMaxSplitRows * kMaxNW) != cudaSuccess ||
+      cudaMalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
+      cudaMalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
+      cudaMalloc(&c->tab.seeds, sizeof(uint32_t) * kMaxW32 * k) != cudaSuccess ||
+      cudaMalloc(&c->ctl, sizeof(LevelCtl)) != cudaSuccess ||
+      cudaMalloc(&c->special, sizeof(unsigned int)) != cudaSuccess ||
+      cudaMalloc(&c->d_blocks, sizeof(Block) * 2 * Ctx::kMaxBlocks) != cudaSuccess ||
+      cudaMallocHost(&c->h_ctl, sizeof(LevelCtl)) != cudaSuccess ||
+      cudaMallocHost(&c->h_blocks, sizeof(Block) * 2 * Ctx::kMaxBlocks) != cudaSuccess)
+    return fail(std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError()));
+  cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
+  if (c->P.empty() && c->N.empty()) {
+    // nothing to precompute: only the trivial case P = {} applies
+    c->tab.n = 0;
+    *out = c.release();
+    return REI_OK;
+  }
+  std::string err;
+  if (!run_precompute(c->P, c->N, (int)k, c->stream, c->tab, err, &c->launches)) {
+    g_init_error = err;
+    return err.find("|IC|") != std::string::npos || err.find("splits") != std::string::npos ? REI_EINVAL
+                                                                                              : REI_ECUDA;
+  }
+  for (auto& w : c->P) c->h2d_bytes += w.size() + 4;
+  for (auto& w : c->N) c->h2d_bytes += w.size() + 4;
+  c->d2h_bytes += 64 + 8ull * c->tab.n;  // table summary + IC keys
+  c->W32 = next_pow2_words(c->tab.n);
+  c->mode = (c->tab.n <= 32) ? DEDUP_BITMAP : (c->W32 == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
+  if (!c->budget) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    c->budget = (uint64_t)(0.8 * (double)fr);
+  }
+  if (c->mode == DEDUP_BITMAP) {
+    c->bitmap_words = std::max<uint64_t>(1, (1ull << c->tab.n) / 32);
+    if (cudaMalloc(&c->bitmap, c->bitmap_words * 4) != cudaSuccess) return fail("bitmap allocation failed");
+    c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
+  }
+  uint64_t cap0 = 1ull << 20;
+  if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(cap0, (1ull << c->tab.n) + 64);
+  cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, c->budget / bytes_per_entry(c.get())));
+  if (alloc_arena(c.get(), cap0, 0, 0) != REI_OK) return fail(c->err);
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail("init sync failed");
+  *out = c.release();
+  return REI_OK;
+}
+
+rei_status rei_solve(void* ctx, uint32_t max_cost, rei_result* out) {
+  if (!ctx) return REI_EINVAL;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  cudaSetDevice(c->device);
+  c->err.clear();
+  const auto t0 = std::chrono::steady_clock::now();
+  rei_status s;
+  if (c->tab.n == 0 && !c->P.empty()) {
+    s = REI_EINVAL;
+  } else {
+    s = rei::solve_impl(c, max_cost);
+  }
+  c->result.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  c->result.regex = c->regex.c_str();
+  uint64_t uniq = 0;
+  for (auto& st : c->stats) uniq += st.unique;
+  c->result.unique = uniq;
+  if (out) *out = c->result;
+  return s;
+}
+
+rei_status rei_level_stats(const void* ctx, rei_level_stat* buf, size_t cap, size_t* n_out) {
+  if (!ctx) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (n_out) *n_out = c->stats.size();
+  for (size_t i = 0; i < c->stats.size() && i < cap && buf; ++i) buf[i] = c->stats[i];
+  return REI_OK;
+}
+
+rei_status rei_kernel_stats(const void* ctx, rei_kernel_class k, uint64_t* launches, double* ms) {
+  if (!ctx || k < 0 || k >= REI_K_COUNT) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (launches) *launches = c->k_launches[k];
+  if (ms) *ms = c->k_ms[k];
+  return REI_OK;
+}
+
+rei_status rei_reset_kernel_stats(void* ctx) {
+  if (!ctx) return REI_EINVAL;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  for (int i = 0; i < REI_K_COUNT; ++i) { c->k_launches[i] = 0; c->k_ms[i] = 0; }
+  c->launches = 0;
+  return REI_OK;
+}
+
+uint64_t rei_launch_count(const void* ctx) { return ctx ? static_cast<const Ctx*>(ctx)->launches : 0; }
+
+rei_status rei_transfer_bytes(const void* ctx, uint64_t* h2d, uint64_t* d2h) {
+  if (!ctx) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (h2d) *h2d = c->h2d_bytes;
+  if (d2h) *d2h = c->d2h_bytes;
+  return REI_OK;
+}
+
+const char* rei_last_error(const void* ctx) {
+  return ctx ? static_cast<const Ctx*>(ctx)->err.c_str() : rei::g_init_error.c_str();
+}
+const char* rei_last_init_error(void) { return rei::g_init_error.c_str(); }
+
+void rei_destroy(void* ctx) { delete static_cast<Ctx*>(ctx); }
+
+rei_status rei_ic(const void* ctx, uint32_t k, char* buf, size_t cap, uint32_t* n_ic) {
+  if (!ctx) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (n_ic) *n_ic = (uint32_t)c->tab.n;
+  if (!buf) return REI_OK;
+  if (k >= (uint32_t)c->tab.n) return REI_EINVAL;
+  const unsigned long long key = c->tab.ic_keys[k];
+  const int len = (int)(key >> 58);
+  unsigned long long v = key & ((1ull << 58) - 1);
+  if ((size_t)len + 1 > cap) return REI_EINVAL;
+  const size_t base = c->alphabet.size();
+  for (int i = len - 1; i >= 0; --i) {
+    buf[i] = c->alphabet[v % base];
+    v /= base;
+  }
+  buf[len] = 0;
+  return REI_OK;
+}
+
+rei_status rei_splits(const void* ctx, uint32_t w, uint32_t* pairs, size_t cap, uint32_t* count) {
+  if (!ctx) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  if (w >= (uint32_t)c->tab.n) return REI_EINVAL;
+  uint32_t m = 0;
+  if (cudaMemcpy(&m, c->tab.nsplit + w, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return REI_ECUDA;
+  if (count) *count = m;
+  for (uint32_t kk = 0; kk < m && kk < cap && pairs; ++kk) {
+    uint32_t sp = 0;
+    if (cudaMemcpy(&sp, c->tab.split + (size_t)kk * rei::kMaxNW + w, 4, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return REI_ECUDA;
+    pairs[2 * kk] = sp >> 16;
+    pairs[2 * kk + 1] = sp & 0xffff;
+  }
+  return REI_OK;
+}
+
+rei_status rei_masks(const void* ctx, uint32_t* pos, uint32_t* neg) {
+  if (!ctx) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  for (int q = 0; q < c->W32; ++q) {
+    if (pos) pos[q] = c->tab.pos[q];
+    if (neg) neg[q] = c->tab.neg[q];
+  }
+  return REI_OK;
+}
+
+rei_status rei_level_cs(const void* ctx, uint32_t cost, uint32_t* out, size_t cap, size_t* count) {
+  if (!ctx) return REI_EINVAL;
+  const Ctx* c = static_cast<const Ctx*>(ctx);
+  auto it = c->levels.find((int)cost);
+  const uint64_t m = it == c->levels.end() ? 0 : it->second.size;
+  if (count) *count = m;
+  if (!out || !m) return REI_OK;
+  const uint64_t take = std::min<uint64_t>(m, cap);
+  if (cudaMemcpy(out, c->arena + it->second.begin * c->W32, take * 4ull * c->W32, cudaMemcpyDeviceToHost) !=
+      cudaSuccess)
+    return REI_ECUDA;
+  return REI_OK;
+}
+
+rei_status rei_entry_regex(const void* ctx, uint32_t cost, uint64_t i, char* buf, size_t cap) {
+  if (!ctx) return REI_EINVAL;
+  Ctx* c = const_cast<Ctx*>(static_cast<const Ctx*>(ctx));
+  auto it = c->levels.find((int)cost);
+  if (it == c->levels.end() || i >= it->second.size) return REI_EINVAL;
+  std::string s;
+  int pr;
+  if (!rei::rebuild_entry(c, (int)cost, i, s, pr, 0)) return REI_ECUDA;
+  if (s.size() + 1 > cap) return REI_EINVAL;
+  memcpy(buf, s.c_str(), s.size() + 1);
+  return REI_OK;
+}
+
+rei_status rei_cs_ops(void* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out, size_t count) {
+  if (!ctx || !a || !out) return REI_EINVAL;
+  Ctx* c = static_cast<Ctx*>(ctx);
+  if (!count) return REI_OK;
+  const size_t bytes = count * 4ull * c->W32;
+  uint32_t *da = nullptr, *db = nullptr, *dout = nullptr;
+  CUDA_OK(c, cudaMalloc(&da, bytes));
+  CUDA_OK(c, cudaMalloc(&db, bytes));
+  CUDA_OK(c, cudaMalloc(&dout, bytes));
+  CUDA_OK(c, cudaMemcpyAsync(da, a, bytes, cudaMemcpyHostToDevice, c->stream));
+  if (b) CUDA_OK(c, cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, c->stream));
+  rei::LevelParams p;
+  rei::fill_params(c, p);
+  rei::EventPair ep;
+  c->begin_kernel(REI_K_OTHER, ep);
+  int n = rei::launch_ops(c->W32, p, op, da, b ? db : nullptr, dout, count, c->stream);
+  c->end_kernel(ep, n);
+  CUDA_OK(c, cudaGetLastError());
+  CUDA_OK(c, cudaMemcpyAsync(out, dout, bytes, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->collect_events(nullptr);
+  cudaFree(da); cudaFree(db); cudaFree(dout);
+  return REI_OK;
+}
+
+void rei_partition(uint64_t total, int G, int g, uint64_t* begin, uint64_t* end) {
+  if (G <= 0) G = 1;
+  const uint64_t b = total / (uint64_t)G * (uint64_t)g + std::min<uint64_t>((uint64_t)g, total % (uint64_t)G);
+  const uint64_t len = total / (uint64_t)G + ((uint64_t)g < total % (uint64_t)G ? 1 : 0);
+  if (begin) *begin = b;
+  if (end) *end = b + len;
+}
+
+}  // extern "C"

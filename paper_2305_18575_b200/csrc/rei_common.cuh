@@ -1,0 +1,84 @@
+// rei_common.cuh -- device/host structures of the B200 REI hot path.
+//
+// Layout in HBM:
+//   arena   : the language cache: one CS per entry,
+//             W32 32-bit words, entries of one cost level contiguous, levels in
+//             increasing cost, write-once.
+//   bp      : one u64 back-pointer per entry = the candidate's rank in its level's
+//             flattened block space (Q, S, C by L ascending, U by L ascending,
+//             row-major); the host decodes it with the level plan.
+//   tarena  : the same levels bit-transposed in slabs of 32 CSs: slab word v has
+//             bit t = CS_t[v] (the "sliced" operand layout of the concat kernel).
+//   dedup   : bitmap over all 2^n CSs (n <= 32) or an open-addressing hash set.
+#pragma once
+#include <cstdint>
+
+namespace rei {
+
+constexpr int kMaxW32 = 16;        // CS words: |IC| <= 512 bits
+constexpr int kMaxNW = 32 * kMaxW32;
+constexpr int kMaxSplitRows = 64;  // max proper splits of one IC word (|w| - 1)
+
+enum BlockKind : uint32_t { BK_Q = 0, BK_S = 1, BK_C = 2, BK_U = 3 };
+
+// One operand block of a cost level (Alg. 1 lines 5-8, Alg. 2 line 2).
+struct Block {
+  uint32_t kind;      // BlockKind
+  uint32_t slice_a;   // C/U: 1 => the A (left) operand is the sliced side, B uniform
+  uint32_t tri;       // U with L == R: only i < j
+  uint32_t pad;
+  uint64_t a_base, b_base;  // arena index of the first entry of level L / R
+  uint64_t a_slab, b_slab;  // tarena slab index of level L / R
+  uint64_t na, nb;          // |lvl(L)|, |lvl(R)|
+  uint64_t cand_off;        // rank of the first candidate of this block within the level
+  uint64_t cand_count;
+  uint64_t item_off;        // first work item of this block (pair kernels)
+  uint64_t u_tiles, s_tiles;  // work-item grid: uniform tiles x slab tiles
+  uint64_t tu, ts;            // uniform operands / slabs (of 32) per work item
+};
+
+// Per-level control block, reset before each level (one 64-byte line).
+struct LevelCtl {
+  unsigned long long found_rank;  // min rank of a precise candidate; ~0 = none
+  unsigned long long count;       // new CSs appended to the level
+  unsigned long long evaluated;   // candidates evaluated (items finished)
+  unsigned int overflow;          // arena / hash capacity exceeded
+  unsigned int special_seen;      // hash64 mode: the sentinel key was inserted
+  unsigned long long pad[4];
+};
+
+enum DedupMode : int { DEDUP_BITMAP = 0, DEDUP_HASH64 = 1, DEDUP_HASHIDX = 2 };
+
+struct Dedup {
+  int mode;
+  int pad;
+  uint32_t* bitmap;                 // DEDUP_BITMAP: 2^n bits
+  unsigned long long* table;        // DEDUP_HASH64 / DEDUP_HASHIDX
+  unsigned long long mask;          // slots - 1
+  unsigned int* special;            // DEDUP_HASH64: persistent "all-ones key present" flag
+};
+
+struct LevelParams {
+  const uint32_t* arena;      // CS arena (read: operand levels)
+  uint32_t* arena_out;        // same buffer (write: level c)
+  const uint32_t* tarena;     // transposed slabs
+  unsigned long long* bp;     // back-pointers
+  const Block* blocks;
+  uint32_t nblocks;
+  uint32_t n;                 // |IC|
+  uint32_t maxk;              // max proper splits per word
+  uint32_t max_errors;        // allowed-error budget (misclassified examples)
+  uint32_t exact;             // 1 = precise test, 0 = allowed-error test
+  uint32_t early_exit;        // 1 = stop at the first precise candidate
+  uint64_t total_items;
+  uint64_t out_base;          // arena index of the first entry of level c
+  uint64_t cap;               // arena capacity in entries
+  const uint32_t* split;      // [k][kMaxNW] packed (u << 16) | v proper splits
+  const uint32_t* nsplit;     // [kMaxNW] number of proper splits per word
+  LevelCtl* ctl;
+  Dedup dedup;
+  uint32_t pos[kMaxW32];
+  uint32_t neg[kMaxW32];
+};
+
+}  // namespace rei

@@ -1,0 +1,46 @@
+// rei_host.h -- host-side declarations shared by the .cu translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "rei_common.cuh"
+
+namespace rei {
+
+// Device-resident staged precompute (owned by the context).
+struct DeviceTables {
+  int n = 0;        // |IC|
+  int maxk = 0;     // max proper splits of one word
+  int maxlen = 0;   // longest IC word
+  uint32_t* split = nullptr;     // [kMaxSplitRows][kMaxNW]
+  uint32_t* nsplit = nullptr;    // [kMaxNW]
+  uint32_t* word_len = nullptr;  // [kMaxNW]
+  uint32_t* seeds = nullptr;     // [k][kMaxW32]
+  uint32_t pos[kMaxW32] = {0};
+  uint32_t neg[kMaxW32] = {0};
+  std::vector<unsigned long long> ic_keys;  // host copy for introspection / printing
+};
+
+bool run_precompute(const std::vector<std::vector<uint8_t>>& P, const std::vector<std::vector<uint8_t>>& N,
+                    int k, cudaStream_t st, DeviceTables& t, std::string& err, uint64_t* launches);
+
+// Kernel launchers (levels.cu).  Each returns the number of kernels launched.
+int launch_seeds(int W32, const LevelParams& p, const uint32_t* seeds, int nsym, cudaStream_t st);
+int launch_unary(int W32, const LevelParams& p, uint64_t n_q, uint64_t n_s, uint64_t a_base_q,
+                 uint64_t a_base_s, uint64_t off_s, cudaStream_t st);
+int launch_concat(int W32, const LevelParams& p, cudaStream_t st);
+int launch_union(int W32, const LevelParams& p, cudaStream_t st);
+int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t count, uint32_t* tarena,
+                     uint64_t slab_base, cudaStream_t st);
+int launch_rehash(int W32, const LevelParams& p, uint64_t count, cudaStream_t st);
+int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
+               uint64_t count, cudaStream_t st);
+
+// Work-item tiling of the pair kernels (uniform operands x slabs of 32).
+constexpr int kTileU = 64;    // uniform operands per work item
+constexpr int kTileS = 4;     // slabs (of 32 sliced operands) per work item
+
+}  // namespace rei
