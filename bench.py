@@ -1,0 +1,353 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 REI hot path (BASELINE.json metric: candidate REs/sec and
+time-to-minimal-RE on the hardest benchmark).
+
+Default workload (BASELINE configs[4], the paper's hardest known-spec class):
+Table 1 row 1 = the Section 5 specification, binary alphabet,
+cost homomorphism (1,1,1,1,1); one *step* = one full ``rei_solve`` from level 1 to
+the first level holding a precise CS (c* = 28), i.e. one pass of every
+hot-path row (Q, S, concat, union, precision test, dedup, append, reconstruction).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun (N > 1) every rank solves the workload independently (replicas;
+"scaling": "weak"); the time is the max over ranks.  ``--impl reference`` times the
+CPU oracle (oracle/, the only reference this tier has) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import specgen  # noqa: E402
+
+# ------------------------------------------------------------------ workloads
+
+WORKLOADS = {
+    # name: (spec, max_cost, description)
+    "table1-row1": (specgen.TABLE1_ROW1, 40,
+                    "Table 1 row 1 / Section 5 spec (P:1345, P:1779-1782), costs (1,1,1,1,1), "
+                    "solve to the minimal precise regex (c*=28, P:1798)"),
+    "table1-row8": (specgen.TABLE1_ROW8, 400,
+                    "Table 1 row 8 (P:1352): same spec, costs (10,10,10,1,10), solve to c*"),
+    "c1-toy": (specgen.C1_TOY, 40, "BASELINE configs[0] paper-style toy"),
+}
+# Paper numbers for the same workload on its own hardware (context):
+PAPER = {
+    "table1-row1": {"reps": 26774099142, "gpu_s": 4.9512, "cpu_s": 5080.7850,
+                    "hw": "Colab A100-SXM4-40GB (P:1147-1153)"},
+    "table1-row8": {"reps": 23349552935, "gpu_s": 4.9096, "cpu_s": 4519.9456,
+                    "hw": "Colab A100-SXM4-40GB (P:1147-1153)"},
+}
+ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8}   # cpu_baseline sample
+REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8}  # --impl reference step
+
+METRIC = "candidate REs/sec"
+UNIT = "cand/s"
+
+# Algorithmic integer lane-ops per candidate (SURVEY 8(d) model):
+#   union  ~ 7*W32 + 12   (OR, precision test, hash/probe address, compare)
+#   concat ~ union + S_in_active/32 + 2*W32 (bit-sliced fold + epsilon terms)
+def ops_per_candidate(kind: str, w32: int, s_in: int) -> float:
+    base = 7 * w32 + 12
+    if kind == "concat":
+        return base + (s_in / 2) / 32 + 2 * w32
+    return base
+
+
+THROTTLE_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = os.path.join("/tmp", f"rei_clocks_{os.getpid()}.csv")
+
+    def start(self):
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,power.draw",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 3:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+                bits = int(parts[2], 16)
+            except ValueError:
+                continue
+            if bits & 0x1:  # idle samples are not "under load"
+                continue
+            sm.append(s)
+            mx.append(m)
+            for b, name in THROTTLE_BITS.items():
+                if bits & b:
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        return json.load(open(path)), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def oracle_rate(spec, max_cost):
+    import oracle
+    t0 = time.perf_counter()
+    r = oracle.Oracle.from_spec(spec).solve(max_cost)
+    dt = time.perf_counter() - t0
+    return r.cand_complete, dt, r
+
+
+# ------------------------------------------------------------------ reference arm
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    spec, _, desc = WORKLOADS[args.workload]
+    mc = REFERENCE_STEP_COST[args.workload]
+    for _ in range(args.warmup):
+        oracle_rate(spec, mc)
+    cands, secs = 0, 0.0
+    for _ in range(args.steps):
+        c, dt, _ = oracle_rate(spec, mc)
+        cands += c
+        secs += dt
+    value = cands / secs
+    sample = (f"oracle (single-threaded C++, oracle/rei_oracle.cpp) levels 1..{mc} of {args.workload} "
+              f"per step ({cands // args.steps} candidates)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * secs / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": {"workload": args.workload, "description": desc,
+                                        "sample_max_cost": mc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2305_18575_b200 import Solver, build
+
+    build.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec, max_cost, desc = WORKLOADS[args.workload]
+    stream = torch.cuda.Stream(device=dev)
+    solver = Solver.from_spec(spec, device=local_rank, stream=stream)
+    # L2 flush buffer (> 126 MB L2), written between timed steps
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        r = solver.solve(max_cost)
+        assert r.status == "found", r.status
+    torch.cuda.synchronize()
+    solver.reset_kernel_stats()
+    launches0 = solver.launch_count()
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    step_ms, cands, results = [], 0, []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.add_(1)  # write > L2 between timed steps
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = solver.solve(max_cost)
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        barrier()
+        step_ms.append(e0.elapsed_time(e1))
+        cands += r.candidates
+        results.append(r)
+    clocks = sampler.stop()
+    launches = solver.launch_count() - launches0
+    kstats = solver.kernel_stats()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        cc = torch.tensor([cands], dtype=torch.float64, device=dev)
+        dist.all_reduce(cc, op=dist.ReduceOp.SUM)
+        all_cands = float(cc.item())
+    else:
+        all_cands = float(cands)
+    value = all_cands / (total_ms / 1000.0)
+
+    # ---- roofline of the dominant kernel (CUDA events on the launching stream)
+    dom = max(("concat", "union", "unary", "transpose"), key=lambda k: kstats[k][1])
+    dom_launches, dom_ms = kstats[dom]
+    evaluated = 0
+    for rr in results:
+        for l in rr.levels:
+            evaluated += {"concat": l.eval_c, "union": l.eval_u}.get(dom, l.evaluated)
+    w32 = results[0].cs_words
+    s_in = sum(max(0, len(w) - 1) for w in solver.ic())
+    peaks, peaks_kind = load_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    alu_peak = 64 * 148 * sm_mhz * 1e6  # INT32 ALU-pipe lane-ops/s (B300_MICROARCH rt_SMSP=2)
+    opc = ops_per_candidate(dom, w32, s_in)
+    achieved = (evaluated / dom_launches) * opc / (dom_ms / dom_launches / 1000.0) if dom_launches else 0.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath))
+        traffic = t.get(args.workload, {}).get(dom)
+    roofline = {
+        "bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
+        "frac": achieved / alu_peak, "traffic": traffic, "kernel": f"k_{dom}<W32={w32}>",
+        "ops_per_candidate": opc, "launches": dom_launches, "avg_launch_ms": dom_ms / max(1, dom_launches),
+        "share_of_step": dom_ms / total_ms if world == 1 else None,
+        "peak_source": f"64 INT32 lane-ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
+        "hbm_peak_gbs": peaks.get("hbm_gbs"),
+    }
+
+    # ---- end to end through the public API with host buffers (rei_init + rei_solve + result)
+    e2e_s, e2e_cands, h2d, d2h = 0.0, 0, 0, 0
+    for _ in range(max(1, min(args.steps, 5))):
+        with torch.cuda.stream(stream):
+            flush.add_(1)
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        s2 = Solver.from_spec(spec, device=local_rank, stream=stream)
+        r2 = s2.solve(max_cost)
+        _ = r2.regex  # result already copied to the host by rei_solve
+        torch.cuda.synchronize()
+        e2e_s += time.perf_counter() - t0
+        e2e_cands += r2.candidates
+        hb, db = s2.transfer_bytes()
+        h2d += hb
+        d2h += db
+        s2.close()
+    n_e2e = max(1, min(args.steps, 5))
+    e2e = {"value": e2e_cands / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // n_e2e,
+           "d2h_bytes_per_step": d2h // n_e2e,
+           "time_to_minimal_re_ms": 1000 * e2e_s / n_e2e,
+           "note": "rei_init (host strings -> device precompute) + rei_solve + result, host wall clock"}
+
+    # ---- CPU oracle baseline (rank 0, N=1 only, bounded sample)
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        mc = ORACLE_SAMPLE_COST[args.workload]
+        c, dt, _ = oracle_rate(spec, mc)
+        cpu_baseline = {"value": c / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                        "sample": f"oracle/rei_oracle.cpp levels 1..{mc} of {args.workload}: "
+                                  f"{c} candidates in {dt:.1f} s on 1 host core"}
+
+    paper = PAPER.get(args.workload)
+    vs = None
+    if paper:
+        vs = value / (paper["reps"] / paper["gpu_s"])
+    r0 = results[-1]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": vs, "dtype": "u32", "data": "synthetic",
+        "config": {
+            "workload": args.workload, "description": desc, "max_cost": max_cost,
+            "n_ic": r0.n_ic, "cs_bits": 32 * r0.cs_words, "cstar": r0.cost, "regex": r0.regex,
+            "candidates_per_step": cands / args.steps,
+            "candidates_through_last_complete_level": r0.cand_complete,
+            "time_to_minimal_re_ms": statistics.median(step_ms),
+            "l2": f"{args.flush_mb} MiB buffer written between timed steps (L2 flush)",
+            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "paper_context": paper,
+            "vs_baseline_note": "value / paper's |REs| per GPU-second on A100 for this spec; the paper's "
+                                "|REs| counting convention differs from reading A9 (DESIGN.md)" if paper else None,
+        },
+        "roofline": roofline,
+        "cpu_baseline": cpu_baseline,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="table1-row1")
+    ap.add_argument("--flush-mb", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        return run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -85,6 +85,7 @@ typedef struct {
   uint64_t cand_q, cand_s, cand_c, cand_u; /* candidates by outermost constructor (A9)  */
   uint64_t unique;             /* new unique CSs appended at this level                 */
   uint64_t evaluated;          /* candidates actually evaluated (== sum of cand_* when complete) */
+  uint64_t eval_c, eval_u;     /* of which by the concatenation / union kernels        */
   double ms;                   /* device time of the level (CUDA events)                */
 } rei_level_stat;
 

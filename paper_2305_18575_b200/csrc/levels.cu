@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "rei_common.cuh"
 #include "rei_host.h"
@@ -221,13 +222,14 @@ __device__ __forceinline__ unsigned long long key64(const uint32_t (&cs)[W]) {
 }
 
 // Batched candidate processing: precision test on every candidate (reading A11),
-// guaranteed duplicates skipped, G probes issued before any is resolved.
-template <int W, int G>
+// guaranteed duplicates skipped, G probes issued before any is resolved.  The
+// candidate's rank (its back-pointer) is computed only when it is needed.
+template <int W, int G, class RankF>
 __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
-                                              const bool (&skip)[G], const unsigned long long (&rank)[G]) {
+                                              const bool (&skip)[G], RankF rank_of) {
 #pragma unroll
   for (int g = 0; g < G; ++g)
-    if (valid[g] && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, rank[g]);
+    if (valid[g] && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, rank_of(g));
 
   if (p.dedup.mode == DEDUP_BITMAP) {
     uint32_t word[G];
@@ -241,7 +243,7 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
       const uint32_t bit = 1u << (cs[g][0] & 31);
       if (!(word[g] & bit)) {
         const uint32_t old = atomicOr(&p.dedup.bitmap[cs[g][0] >> 5], bit);
-        if (!(old & bit)) append<W>(p, cs[g], rank[g]);
+        if (!(old & bit)) append<W>(p, cs[g], rank_of(g));
       }
     }
   } else if (p.dedup.mode == DEDUP_HASH64) {
@@ -257,15 +259,43 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
     for (int g = 0; g < G; ++g) {
       if (val[g] != key[g] || key[g] == kEmpty64) {
         const bool need = valid[g] && !skip[g];
-        if (need && insert_hash64(p, key[g], slot[g], val[g])) append<W>(p, cs[g], rank[g]);
+        if (need && insert_hash64(p, key[g], slot[g], val[g])) append<W>(p, cs[g], rank_of(g));
       }
     }
   } else {
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      if (valid[g] && !skip[g]) insert_indexed<W>(p, cs[g], rank[g], true, 0);
+      if (valid[g] && !skip[g]) insert_indexed<W>(p, cs[g], rank_of(g), true, 0);
   }
 }
+
+// Rotation-based 32x32 transpose step constants for this lane: stage j rotates the
+// partner word left by (lane & j ? 32 - j : j) and keeps the lane's own bits under km.
+struct TransposeLane {
+  uint32_t rot[5], km[5];
+  __device__ __forceinline__ explicit TransposeLane(uint32_t lane) {
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const uint32_t j = 16u >> s;
+      const uint32_t m = (j == 16) ? 0x0000FFFFu : (j == 8) ? 0x00FF00FFu
+                       : (j == 4) ? 0x0F0F0F0Fu : (j == 2) ? 0x33333333u : 0x55555555u;
+      const bool hi = (lane & j) != 0;
+      rot[s] = hi ? 32u - j : j;
+      km[s] = hi ? ~m : m;
+    }
+  }
+  // Same matrix transpose as transpose32(), 3 instructions per stage: SHFL, SHF.W, LOP3.
+  __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+      const uint32_t j = 16u >> s;
+      const uint32_t y = __shfl_xor_sync(kFull, x, j);
+      const uint32_t yr = __funnelshift_l(y, y, rot[s]);  // rotate left
+      x = (x & km[s]) | (yr & ~km[s]);
+    }
+    return x;
+  }
+};
 
 // ---- work-item decode (blocks staged in shared memory)
 __device__ __forceinline__ int find_block(const Block* blocks, int nb, unsigned long long item) {
@@ -395,18 +425,138 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
           for (int q = 0; q < W; ++q) cs[g][q] = transpose32(acc[q], lane);
           valid[g] = active && lane_ok;
           skip[g] = cs_equal<W>(cs[g], x);  // equals a cached operand: old
-          const unsigned long long i = slice_a ? sj : ui;
-          const unsigned long long j = slice_a ? ui : sj;
-          rank[g] = blk.cand_off + i * blk.nb + j;
           evaluated += valid[g] ? 1u : 0u;
         }
-        process_batch<W, G>(p, cs, valid, skip, rank);
+        const unsigned long long cand_off = blk.cand_off, nb = blk.nb;
+        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+          const unsigned long long ui = u + g;
+          return cand_off + (slice_a ? sj * nb + ui : ui * nb + sj);
+        });
       }
       if (!kShfl) __syncwarp();
-      if (found_and_stop(p)) break;
     }
     const uint32_t tot = __reduce_add_sync(kFull, evaluated);
-    if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
+    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
+  }
+}
+
+// ============================================================================
+// Concatenation fast path for W32 <= 2 (|IC| <= 64) and words with <= MAXK proper
+// splits.  Same arithmetic as k_concat, reorganised for instruction-level
+// parallelism:
+//   * per lane, the split table of its word(s) lives in registers as
+//     (uniform-side bit mask, sliced-side source word) pairs, fixed per orientation
+//     (SLICE_A: the left operand is the sliced one);
+//   * per slab, the shuffled slab words t_k = T[src_k] are fetched once and reused
+//     by every uniform operand of the work item (up to 64 of them);
+//   * per group the fold is MAXK predicated ORs; the transpose is 3 instructions
+//     per stage (SHFL, funnel rotate, LOP3); G groups are independent chains.
+template <int W, int MAXK, bool SLICE_A>
+__global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
+  static_assert(W <= 2, "fast path is for one- and two-word CSs");
+  constexpr int NW = 32 * W;
+  constexpr int G = (W == 1) ? 8 : 4;  // two-word CSs: fewer groups in flight, no spills
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
+  uint32_t* s_src = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);  // [MAXK][NW]
+  for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  for (int i = threadIdx.x; i < MAXK * NW; i += blockDim.x) {
+    const uint32_t sp = p.split[(size_t)(i / NW) * kMaxNW + (i % NW)];
+    s_src[i] = SLICE_A ? (sp >> 16) : (sp & 0xffffu);  // word of the sliced slab
+  }
+  __syncthreads();
+
+  const uint32_t lane = lane_id();
+  const TransposeLane tr(lane);
+  // split masks: bit of the uniform operand that enables split k of word q*32+lane
+  uint32_t mlo[W][MAXK], mhi[W][MAXK];
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    const uint32_t w = q * 32 + lane;
+    const uint32_t ns = p.nsplit[w];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+      const bool ok = (uint32_t)k < ns;
+      const uint32_t sp = ok ? p.split[(size_t)k * kMaxNW + w] : 0u;
+      const uint32_t fixed = SLICE_A ? (sp & 0xffffu) : (sp >> 16);
+      mlo[q][k] = (ok && fixed < 32) ? (1u << fixed) : 0u;
+      mhi[q][k] = (ok && fixed >= 32) ? (1u << (fixed & 31)) : 0u;
+    }
+  }
+  const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+
+  for (unsigned long long item = gwarp; item < p.total_items; item += nwarps) {
+    if (found_and_stop(p)) break;
+    const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
+    const unsigned long long local = item - blk.item_off;
+    const unsigned long long ut = local / blk.s_tiles, st = local % blk.s_tiles;
+    const unsigned long long nu = SLICE_A ? blk.nb : blk.na;
+    const unsigned long long ns = SLICE_A ? blk.na : blk.nb;
+    const uint32_t* ubase = p.arena + (SLICE_A ? blk.b_base : blk.a_base) * W;
+    const unsigned long long slab_base = SLICE_A ? blk.a_slab : blk.b_slab;
+    const unsigned long long u0 = ut * blk.tu, u1 = min(u0 + blk.tu, nu);
+    const unsigned long long nslabs = (ns + 31) / 32;
+    const unsigned long long s0 = st * blk.ts, s1 = min(s0 + blk.ts, nslabs);
+    const unsigned long long cand_off = blk.cand_off, nb = blk.nb;
+    uint32_t evaluated = 0;
+
+    for (unsigned long long s = s0; s < s1; ++s) {
+      uint32_t T[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) T[q] = p.tarena[(slab_base + s) * NW + q * 32 + lane];
+      const uint32_t Teps = __shfl_sync(kFull, T[0], 0);
+      uint32_t tk[W][MAXK];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) {
+          const uint32_t src = s_src[k * NW + q * 32 + lane];
+          const uint32_t t0 = __shfl_sync(kFull, T[0], src & 31);
+          if (W == 2) {
+            const uint32_t t1 = __shfl_sync(kFull, T[W - 1], src & 31);
+            tk[q][k] = (src >> 5) ? t1 : t0;
+          } else {
+            tk[q][k] = t0;
+          }
+        }
+      }
+      const unsigned long long sj = s * 32 + lane;
+      const bool lane_ok = sj < ns;
+
+      for (unsigned long long u = u0; u < u1; u += G) {
+        uint32_t cs[G][W];
+        bool valid[G], skip[G];
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const bool active = u + g < u1;
+          uint32_t x[W];
+#pragma unroll
+          for (int q = 0; q < W; ++q) x[q] = 0;
+          if (active) load_cs<W>(ubase, u + g, x);
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            uint32_t acc = ((x[0] & 1u) ? T[q] : 0u) | (((x[q] >> lane) & 1u) ? Teps : 0u);
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k) {
+              const uint32_t hit = (x[0] & mlo[q][k]) | (W == 2 ? (x[W - 1] & mhi[q][k]) : 0u);
+              acc |= hit ? tk[q][k] : 0u;
+            }
+            cs[g][q] = tr(acc);
+          }
+          valid[g] = active && lane_ok;
+          skip[g] = cs_equal<W>(cs[g], x);
+          evaluated += valid[g] ? 1u : 0u;
+        }
+        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+          const unsigned long long ui = u + g;
+          return cand_off + (SLICE_A ? sj * nb + ui : ui * nb + sj);
+        });
+      }
+    }
+    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
+    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
   }
 }
 
@@ -455,7 +605,6 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
         if (tri && u >= s * 32 + 31) break;  // no j > i left in this slab
         uint32_t cs[G][W];
         bool valid[G], skip[G];
-        unsigned long long rank[G];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           const unsigned long long ui = u + g;
@@ -468,20 +617,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
           }
 #pragma unroll
           for (int q = 0; q < W; ++q) cs[g][q] = x[q] | y[q];
-          const unsigned long long i = slice_a ? sj : ui;
-          const unsigned long long j = slice_a ? ui : sj;
-          valid[g] = active && lane_ok && (!tri || j > i);
+          valid[g] = active && lane_ok && (!tri || sj > ui);
           skip[g] = cs_equal<W>(cs[g], x) || cs_equal<W>(cs[g], y);
-          rank[g] = blk.cand_off +
-                    (tri ? i * blk.na - i * (i + 1) / 2 + (j - i - 1) : i * blk.nb + j);
           evaluated += valid[g] ? 1u : 0u;
         }
-        process_batch<W, G>(p, cs, valid, skip, rank);
+        const unsigned long long cand_off = blk.cand_off, na = blk.na, nb = blk.nb;
+        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+          const unsigned long long ui = u + g;
+          const unsigned long long i = slice_a ? sj : ui;
+          const unsigned long long j = slice_a ? ui : sj;
+          return cand_off + (tri ? i * na - i * (i + 1) / 2 + (j - i - 1) : i * nb + j);
+        });
       }
-      if (found_and_stop(p)) break;
     }
     const uint32_t tot = __reduce_add_sync(kFull, evaluated);
-    if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
+    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_u, (unsigned long long)tot); }
   }
 }
 
@@ -541,7 +691,7 @@ __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long
       rank[0] = off_s + (t - n_q);
     }
     skip[0] = cs_equal<W>(cs[0], x);
-    process_batch<W, 1>(p, cs, valid, skip, rank);
+    process_batch<W, 1>(p, cs, valid, skip, [&](int) { return rank[0]; });
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&p.ctl->evaluated, total);
@@ -557,7 +707,7 @@ __global__ void k_seeds(LevelParams p, const uint32_t* seeds, int nsym) {
     for (int q = 0; q < W; ++q) cs[0][q] = seeds[a * kMaxW32 + q];
     bool valid[1] = {true}, skip[1] = {false};
     unsigned long long rank[1] = {(unsigned long long)a};
-    process_batch<W, 1>(p, cs, valid, skip, rank);
+    process_batch<W, 1>(p, cs, valid, skip, [&](int) { return rank[0]; });
     if (*(volatile unsigned long long*)&p.ctl->found_rank != ~0ull) break;
   }
   p.ctl->evaluated = 0;
@@ -682,8 +832,30 @@ size_t pair_smem(const LevelParams& p, int W) {
   return s;
 }
 
+template <int W, int MAXK, bool SA>
+int launch_concat_fast_t(const LevelParams& p, cudaStream_t st) {
+  const size_t smem = p.nblocks * sizeof(Block) + (size_t)MAXK * 32 * W * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items);
+  k_concat_fast<W, MAXK, SA><<<grid, kWarps * 32, smem, st>>>(p);
+  return 1;
+}
+
+template <int W, bool SA>
+int launch_concat_fast_k(const LevelParams& p, cudaStream_t st) {
+  if (p.maxk <= 1) return launch_concat_fast_t<W, 1, SA>(p, st);
+  if (p.maxk <= 3) return launch_concat_fast_t<W, 3, SA>(p, st);
+  if (p.maxk <= 7) return launch_concat_fast_t<W, 7, SA>(p, st);
+  return launch_concat_fast_t<W, 15, SA>(p, st);
+}
+
 template <int W>
-int launch_concat_t(const LevelParams& p, cudaStream_t st) {
+int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
+  if constexpr (W <= 2) {
+    if (p.maxk <= 15 && !getenv("REI_GENERIC_CONCAT"))
+      return slice_a ? launch_concat_fast_k<W, true>(p, st) : launch_concat_fast_k<W, false>(p, st);
+  }
   const size_t smem = pair_smem(p, W);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_concat<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_for(k_concat<W>, kWarps * 32, smem, kWarps, p.total_items);
@@ -741,8 +913,8 @@ int launch_unary(int W32, const LevelParams& p, uint64_t n_q, uint64_t n_s, uint
   REI_DISPATCH_W(W32, return launch_unary_t<W>(p, n_q, n_s, bq, bs, off_s, st));
 }
 
-int launch_concat(int W32, const LevelParams& p, cudaStream_t st) {
-  REI_DISPATCH_W(W32, return launch_concat_t<W>(p, st));
+int launch_concat(int W32, const LevelParams& p, bool slice_a, cudaStream_t st) {
+  REI_DISPATCH_W(W32, return launch_concat_t<W>(p, slice_a, st));
 }
 
 int launch_union(int W32, const LevelParams& p, cudaStream_t st) {

@@ -78,7 +78,7 @@ struct Ctx {
   unsigned int* special = nullptr;
   LevelCtl* ctl = nullptr;
   LevelCtl* h_ctl = nullptr;  // pinned
-  Block* d_blocks = nullptr;  // [2][kMaxBlocks]
+  Block* d_blocks = nullptr;  // [3][kMaxBlocks]: concat (B sliced), concat (A sliced), union
   Block* h_blocks = nullptr;  // pinned
   static constexpr int kMaxBlocks = 4096;
 
@@ -430,6 +430,14 @@ uint64_t items_of(const std::vector<Block>& v) {
   return v.back().item_off + v.back().u_tiles * v.back().s_tiles;
 }
 
+void renumber_items(std::vector<Block>& v) {
+  uint64_t off = 0;
+  for (Block& b : v) {
+    b.item_off = off;
+    off += b.u_tiles * b.s_tiles;
+  }
+}
+
 rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
   rei_status s = clear_dedup(c);
   if (s != REI_OK) return s;
@@ -556,6 +564,15 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
       c->err = "too many operand blocks in one level";
       return REI_EINVAL;
     }
+    // grow ahead of the level when its new CSs may not fit (a level rarely has more
+    // than ~4x the previous level's new CSs; an overflow still triggers a retry)
+    {
+      const uint64_t prev = c->stats.empty() ? 0 : c->stats.back().unique;
+      const uint64_t expect = std::min<uint64_t>(nq + ns + ncat + nuni, 4 * prev + 1024);
+      if (c->arena_used + expect > c->cap || c->slabs_used + expect / 32 + 2 > c->slab_cap) {
+        if ((s = grow(c, c->arena_used + expect)) != REI_OK && s != REI_OUT_OF_MEMORY) return s;
+      }
+    }
     lv.begin = c->arena_used;
     lv.slab = c->slabs_used;
     rei_level_stat st{};
@@ -567,16 +584,19 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
       fill_params(c, p);
       p.out_base = lv.begin;
       if ((s = reset_ctl(c)) != REI_OK) return s;
-      // operand blocks -> device (one small H2D per level)
-      std::copy(cat.begin(), cat.end(), c->h_blocks);
-      std::copy(uni.begin(), uni.end(), c->h_blocks + Ctx::kMaxBlocks);
-      if (!cat.empty())
-        CUDA_OK(c, cudaMemcpyAsync(c->d_blocks, c->h_blocks, cat.size() * sizeof(Block), cudaMemcpyHostToDevice,
-                                   c->stream));
-      if (!uni.empty())
-        CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + Ctx::kMaxBlocks, c->h_blocks + Ctx::kMaxBlocks,
-                                   uni.size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
-      c->h2d_bytes += (cat.size() + uni.size()) * sizeof(Block);
+      // operand blocks -> device (one small H2D per level).  Concatenation blocks are
+      // split by orientation (left or right operand sliced): one launch each.
+      std::vector<Block> catv[2];
+      for (const Block& b : cat) catv[b.slice_a ? 1 : 0].push_back(b);
+      for (auto& v : catv) renumber_items(v);
+      const std::vector<Block>* lists[3] = {&catv[0], &catv[1], &uni};
+      for (int r = 0; r < 3; ++r) {
+        if (lists[r]->empty()) continue;
+        std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
+        CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, c->h_blocks + r * Ctx::kMaxBlocks,
+                                   lists[r]->size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
+        c->h2d_bytes += lists[r]->size() * sizeof(Block);
+      }
       if (nq + ns) {
         const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
         const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
@@ -585,19 +605,20 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
         int n = launch_unary(c->W32, p, nq, ns, bq, bs, nq, c->stream);
         c->end_kernel(ep, n);
       }
-      if (!cat.empty()) {
+      for (int r = 0; r < 2; ++r) {
+        if (catv[r].empty()) continue;
         LevelParams pc = p;
-        pc.blocks = c->d_blocks;
-        pc.nblocks = (uint32_t)cat.size();
-        pc.total_items = items_of(cat);
+        pc.blocks = c->d_blocks + r * Ctx::kMaxBlocks;
+        pc.nblocks = (uint32_t)catv[r].size();
+        pc.total_items = items_of(catv[r]);
         EventPair ep;
         c->begin_kernel(REI_K_CONCAT, ep);
-        int n = launch_concat(c->W32, pc, c->stream);
+        int n = launch_concat(c->W32, pc, r == 1, c->stream);
         c->end_kernel(ep, n);
       }
       if (!uni.empty()) {
         LevelParams pu = p;
-        pu.blocks = c->d_blocks + Ctx::kMaxBlocks;
+        pu.blocks = c->d_blocks + 2 * Ctx::kMaxBlocks;
         pu.nblocks = (uint32_t)uni.size();
         pu.total_items = items_of(uni);
         EventPair ep;
@@ -627,6 +648,8 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
     const bool complete = !found || (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
     st.complete = complete ? 1 : 0;
     st.evaluated = complete ? (nq + ns + ncat + nuni) : c->h_ctl->evaluated;
+    st.eval_c = complete ? ncat : c->h_ctl->eval_c;
+    st.eval_u = complete ? nuni : c->h_ctl->eval_u;
     c->levels[cost] = lv;
     c->stats.push_back(st);
     if (found) {
@@ -743,9 +766,9 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       cudaMalloc(&c->tab.seeds, sizeof(uint32_t) * kMaxW32 * k) != cudaSuccess ||
       cudaMalloc(&c->ctl, sizeof(LevelCtl)) != cudaSuccess ||
       cudaMalloc(&c->special, sizeof(unsigned int)) != cudaSuccess ||
-      cudaMalloc(&c->d_blocks, sizeof(Block) * 2 * Ctx::kMaxBlocks) != cudaSuccess ||
+      cudaMalloc(&c->d_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess ||
       cudaMallocHost(&c->h_ctl, sizeof(LevelCtl)) != cudaSuccess ||
-      cudaMallocHost(&c->h_blocks, sizeof(Block) * 2 * Ctx::kMaxBlocks) != cudaSuccess)
+      cudaMallocHost(&c->h_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess)
     return fail(std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError()));
   cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
   if (c->P.empty() && c->N.empty()) {
@@ -775,8 +798,10 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     if (cudaMalloc(&c->bitmap, c->bitmap_words * 4) != cudaSuccess) return fail("bitmap allocation failed");
     c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
   }
+  // bitmap mode: at most 2^n distinct CSs exist, so reserve them all up front (up to
+  // 2^28 entries); hash modes start at 2^20 entries and grow ahead of each level.
   uint64_t cap0 = 1ull << 20;
-  if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(cap0, (1ull << c->tab.n) + 64);
+  if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(1ull << 28, (1ull << c->tab.n) + 64);
   cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, c->budget / bytes_per_entry(c.get())));
   if (alloc_arena(c.get(), cap0, 0, 0) != REI_OK) return fail(c->err);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail("init sync failed");

@@ -44,7 +44,9 @@ struct LevelCtl {
   unsigned long long evaluated;   // candidates evaluated (items finished)
   unsigned int overflow;          // arena / hash capacity exceeded
   unsigned int special_seen;      // hash64 mode: the sentinel key was inserted
-  unsigned long long pad[4];
+  unsigned long long eval_c;      // of which by the concat kernel
+  unsigned long long eval_u;      // of which by the union kernel
+  unsigned long long pad[2];
 };
 
 enum DedupMode : int { DEDUP_BITMAP = 0, DEDUP_HASH64 = 1, DEDUP_HASHIDX = 2 };

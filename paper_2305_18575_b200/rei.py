@@ -52,7 +52,8 @@ class _LevelStat(ctypes.Structure):
     _fields_ = [("cost", ctypes.c_uint32), ("complete", ctypes.c_uint32),
                 ("cand_q", ctypes.c_uint64), ("cand_s", ctypes.c_uint64),
                 ("cand_c", ctypes.c_uint64), ("cand_u", ctypes.c_uint64),
-                ("unique", ctypes.c_uint64), ("evaluated", ctypes.c_uint64), ("ms", ctypes.c_double)]
+                ("unique", ctypes.c_uint64), ("evaluated", ctypes.c_uint64),
+                ("eval_c", ctypes.c_uint64), ("eval_u", ctypes.c_uint64), ("ms", ctypes.c_double)]
 
 
 _lib = None
@@ -115,6 +116,8 @@ class LevelStat:
     cand_u: int
     unique: int
     evaluated: int
+    eval_c: int
+    eval_u: int
     ms: float
 
     @property
@@ -210,7 +213,7 @@ class Solver:
         buf = (_LevelStat * max(1, n.value))()
         self._lib.rei_level_stats(self._h, buf, n.value, ctypes.byref(n))
         return [LevelStat(b.cost, bool(b.complete), b.cand_q, b.cand_s, b.cand_c, b.cand_u,
-                          b.unique, b.evaluated, b.ms) for b in buf[:n.value]]
+                          b.unique, b.evaluated, b.eval_c, b.eval_u, b.ms) for b in buf[:n.value]]
 
     def kernel_stats(self) -> Dict[str, Tuple[int, float]]:
         out = {}

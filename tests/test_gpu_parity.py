@@ -153,6 +153,22 @@ def test_search_parity_wide(sp, K):
     compare_search(sp, K)
 
 
+@pytest.mark.parametrize("sp,K", RANDOM_W1[:3] + W2[:2], ids=ids(RANDOM_W1[:3] + W2[:2]))
+def test_generic_concat_kernel_parity(sp, K, monkeypatch):
+    # the generic (any split count) concat kernel, used when a word has > 15 proper
+    # splits, exercised on one- and two-word CSs too
+    monkeypatch.setenv("REI_GENERIC_CONCAT", "1")
+    compare_search(sp, K)
+
+
+@pytest.mark.parametrize("sp", [specgen.Spec("01", ("0" * 20, "1"), ("0" * 19, "11")),
+                                specgen.Spec("01", ("0" * 40, "1"), ("0" * 39, "11"))],
+                         ids=["w1-len20", "w2-len40"])
+def test_long_words_use_generic_kernel(sp):
+    # words with more than 15 proper splits take the generic concat kernel
+    compare_search(sp, 12)
+
+
 @pytest.mark.parametrize("pct", [50, 45, 40, 35, 25, 20, 15])
 def test_allowed_error_parity(pct):
     # Section 5 table rows, REI with allowed error.
