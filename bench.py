@@ -123,6 +123,20 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
+def reduce_over_ranks(total_ms, cands, device, world, sum_work=True):
+    """Device time = max over ranks; work = sum over ranks (replicas) or rank 0's
+    (sharded: every rank reports the same global candidate count)."""
+    if world <= 1:
+        return float(total_ms), float(cands)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(total_ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    c = torch.tensor([float(cands)], dtype=torch.float64, device=device)
+    dist.all_reduce(c, op=dist.ReduceOp.SUM if sum_work else dist.ReduceOp.MAX)
+    return float(t.item()), float(c.item())
+
+
 def load_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -180,7 +194,16 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     spec, max_cost, desc = WORKLOADS[args.workload]
     stream = torch.cuda.Stream(device=dev)
-    solver = Solver.from_spec(spec, device=local_rank, stream=stream)
+    sharded = world > 1 and args.multi == "shard"
+    mkw = {}
+    if sharded:
+        # one sharded search over all ranks: rank 0's ncclUniqueId is
+        # broadcast with torch.distributed; rei_init / rei_solve are then collective
+        from paper_2305_18575_b200 import nccl_unique_id
+        box = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        mkw = dict(world_size=world, rank=rank, nccl_id=box[0])
+    solver = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw)
     # L2 flush buffer (> 126 MB L2), written between timed steps
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
 
@@ -216,16 +239,7 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
     launches = solver.launch_count() - launches0
     kstats = solver.kernel_stats()
-    total_ms = sum(step_ms)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        cc = torch.tensor([cands], dtype=torch.float64, device=dev)
-        dist.all_reduce(cc, op=dist.ReduceOp.SUM)
-        all_cands = float(cc.item())
-    else:
-        all_cands = float(cands)
+    total_ms, all_cands = reduce_over_ranks(sum(step_ms), cands, dev, world, sum_work=not sharded)
     value = all_cands / (total_ms / 1000.0)
 
     # ---- roofline of the dominant kernel (CUDA events on the launching stream)
@@ -264,7 +278,12 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
-        s2 = Solver.from_spec(spec, device=local_rank, stream=stream)
+        mkw2 = {}
+        if sharded:
+            box = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(box, src=0)
+            mkw2 = dict(world_size=world, rank=rank, nccl_id=box[0])
+        s2 = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw2)
         r2 = s2.solve(max_cost)
         _ = r2.regex  # result already copied to the host by rei_solve
         torch.cuda.synchronize()
@@ -297,7 +316,7 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": vs, "dtype": "u32", "data": "synthetic",
+        "scaling": "strong" if sharded else "weak", "vs_baseline": vs, "dtype": "u32", "data": "synthetic",
         "config": {
             "workload": args.workload, "description": desc, "max_cost": max_cost,
             "n_ic": r0.n_ic, "cs_bits": 32 * r0.cs_words, "cstar": r0.cost, "regex": r0.regex,
@@ -305,7 +324,8 @@ def run_ours(args, rank, world, local_rank):
             "candidates_through_last_complete_level": r0.cand_complete,
             "time_to_minimal_re_ms": statistics.median(step_ms),
             "l2": f"{args.flush_mb} MiB buffer written between timed steps (L2 flush)",
-            "parallelism": f"replicas{world}" if world > 1 else "single",
+            "parallelism": (f"shard{world} (level work lists partitioned, NCCL all-gather of new CSs)"
+                            if sharded else f"replicas{world}") if world > 1 else "single",
             "paper_context": paper,
             "vs_baseline_note": "value / paper's |REs| per GPU-second on A100 for this spec; the paper's "
                                 "|REs| counting convention differs from reading A9 (DESIGN.md)" if paper else None,
@@ -330,6 +350,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="table1-row1")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--multi", choices=["shard", "replicas"], default="shard",
+                    help="N > 1: one sharded search (default) or N independent replicas")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -152,6 +152,26 @@ rei_status rei_entry_regex(const void* ctx, uint32_t cost, uint64_t i, char* buf
 rei_status rei_cs_ops(void* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                       size_t count);
 
+/* ---- multi-GPU: the sharded level ----
+ * Every rank holds the full language cache.  Each level's work lists (? and *
+ * operands, concatenation and union work items) are split into contiguous rank
+ * shares (rei_partition); a rank enumerates its share, appends the CSs new to its
+ * dedup set, and the ranks' lists are all-gathered in rank order; every rank then
+ * keeps the first occurrence of each CS (canonical merge), so the caches stay
+ * byte-identical.  found / overflow / counts are combined over all ranks.
+ * Supported for |IC| <= 64 (bitmap and 64-bit-key dedup sets). */
+
+/* One process per GPU: rank 0 creates the id, the caller broadcasts it (e.g. with
+ * torch.distributed) and passes it in rei_options.nccl_unique_id with world_size and
+ * rank; rei_init and rei_solve are then collective over the world. out: 128 bytes. */
+rei_status rei_nccl_unique_id(void* out, size_t cap);
+
+/* Virtual ranks in one process: `ctxs` are G contexts created with world_size <= 1
+ * (any devices, the same specification); rei_solve_group runs them as ranks
+ * 0..G-1 of one sharded search, exchanging through device (peer) copies.  Every
+ * context ends with the same result and identical cache; `out` receives rank 0's. */
+rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_result* out);
+
 /* ---- multi-GPU host logic (pure functions, usable without a GPU) ---- */
 
 /* Contiguous share of a flattened candidate / work-item space of size `total` for

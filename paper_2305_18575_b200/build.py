@@ -12,13 +12,13 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librei_b200.so")
-SOURCES = ["precompute.cu", "levels.cu", "rei_api.cu"]
+SOURCES = ["precompute.cu", "levels.cu", "exchange.cu", "rei_api.cu"]
 HEADERS = ["rei_common.cuh", "rei_host.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--shared",
-         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]
+         "-Xptxas", "-v", "-I", os.path.join(ROOT, "include"), "-ldl"]
 
 
 def _stale() -> bool:

@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
+#include <type_traits>
 
 #include "rei_common.cuh"
 #include "rei_host.h"
@@ -133,10 +134,13 @@ __device__ __forceinline__ void store_cs(uint32_t* __restrict__ arena, uint64_t 
 // Warp-aggregated append of a new CS + back-pointer to level c.
 template <int W>
 __device__ __forceinline__ void append(const LevelParams& p, const uint32_t (&cs)[W], unsigned long long rank) {
-  cg::coalesced_group g = cg::coalesced_threads();
+  // the lanes that reach this point together share one atomicAdd
+  const unsigned mask = __activemask();
+  const int leader = __ffs(mask) - 1;
+  const uint32_t lane = threadIdx.x & 31;
   unsigned long long base = 0;
-  if (g.thread_rank() == 0) base = atomicAdd(&p.ctl->count, (unsigned long long)g.size());
-  base = g.shfl(base, 0) + g.thread_rank();
+  if ((int)lane == leader) base = atomicAdd(&p.ctl->count, (unsigned long long)__popc(mask));
+  base = __shfl_sync(mask, base, leader) + __popc(mask & ((1u << lane) - 1u));
   const unsigned long long idx = p.out_base + base;
   if (idx >= p.cap) {
     p.ctl->overflow = 1;
@@ -224,14 +228,27 @@ __device__ __forceinline__ unsigned long long key64(const uint32_t (&cs)[W]) {
 // Batched candidate processing: precision test on every candidate (reading A11),
 // guaranteed duplicates skipped, G probes issued before any is resolved.  The
 // candidate's rank (its back-pointer) is computed only when it is needed.
+// The dedup structure is a function of the CS width (rei_init): |IC| <= 32 -> bitmap,
+// <= 64 -> 64-bit inline keys, wider -> fingerprint + arena index.
+template <int W> struct DedupOf {
+  static constexpr int mode = (W == 1) ? DEDUP_BITMAP : (W == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
+};
+
+// Precision is tested on the CSs that are new (Alg. 2 lines 16-17): a CS
+// already cached at a lower level cannot be precise, or the search would have stopped
+// there, and a within-level duplicate is tested by the candidate that inserted it.
+template <int W, class RankF>
+__device__ __forceinline__ void on_new(const LevelParams& p, const uint32_t (&cs)[W], RankF rank_of, int g) {
+  const unsigned long long r = rank_of(g);
+  if (satisfies<W>(cs, p)) atomicMin(&p.ctl->found_rank, r);
+  append<W>(p, cs, r);
+}
+
 template <int W, int G, class RankF>
 __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
                                               const bool (&skip)[G], RankF rank_of) {
-#pragma unroll
-  for (int g = 0; g < G; ++g)
-    if (valid[g] && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, rank_of(g));
-
-  if (p.dedup.mode == DEDUP_BITMAP) {
+  constexpr int MODE = DedupOf<W>::mode;
+  if (MODE == DEDUP_BITMAP) {
     uint32_t word[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -243,10 +260,10 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
       const uint32_t bit = 1u << (cs[g][0] & 31);
       if (!(word[g] & bit)) {
         const uint32_t old = atomicOr(&p.dedup.bitmap[cs[g][0] >> 5], bit);
-        if (!(old & bit)) append<W>(p, cs[g], rank_of(g));
+        if (!(old & bit)) on_new<W>(p, cs[g], rank_of, g);
       }
     }
-  } else if (p.dedup.mode == DEDUP_HASH64) {
+  } else if (MODE == DEDUP_HASH64) {
     unsigned long long slot[G], val[G], key[G];
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -259,13 +276,18 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
     for (int g = 0; g < G; ++g) {
       if (val[g] != key[g] || key[g] == kEmpty64) {
         const bool need = valid[g] && !skip[g];
-        if (need && insert_hash64(p, key[g], slot[g], val[g])) append<W>(p, cs[g], rank_of(g));
+        if (need && insert_hash64(p, key[g], slot[g], val[g])) on_new<W>(p, cs[g], rank_of, g);
       }
     }
   } else {
 #pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (valid[g] && !skip[g]) insert_indexed<W>(p, cs[g], rank_of(g), true, 0);
+    for (int g = 0; g < G; ++g) {
+      if (valid[g] && !skip[g]) {
+        const unsigned long long r = rank_of(g);
+        if (insert_indexed<W>(p, cs[g], r, true, 0) && satisfies<W>(cs[g], p))
+          atomicMin(&p.ctl->found_rank, r);
+      }
+    }
   }
 }
 
@@ -283,13 +305,21 @@ struct TransposeLane {
       rot[s] = hi ? 32u - j : j;
       km[s] = hi ? ~m : m;
     }
+    // byte-permute selectors of the 16- and 8-bit stages ({partner:own}, own = bytes 0-3)
+    rot[0] = (lane & 16) ? 0x3276u : 0x5410u;
+    rot[1] = (lane & 8) ? 0x3715u : 0x6240u;
   }
-  // Same matrix transpose as transpose32(), 3 instructions per stage: SHFL, SHF.W, LOP3.
+  // Same matrix transpose as transpose32(): the 16- and 8-bit stages move whole bytes
+  // (one PRMT each, per-lane selector), the 4/2/1-bit stages rotate + merge (SHF, LOP3).
   __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
+    uint32_t y = __shfl_xor_sync(kFull, x, 16);
+    x = __byte_perm(x, y, rot[0]);
+    y = __shfl_xor_sync(kFull, x, 8);
+    x = __byte_perm(x, y, rot[1]);
 #pragma unroll
-    for (int s = 0; s < 5; ++s) {
+    for (int s = 2; s < 5; ++s) {
       const uint32_t j = 16u >> s;
-      const uint32_t y = __shfl_xor_sync(kFull, x, j);
+      y = __shfl_xor_sync(kFull, x, j);
       const uint32_t yr = __funnelshift_l(y, y, rot[s]);  // rotate left
       x = (x & km[s]) | (yr & ~km[s]);
     }
@@ -343,7 +373,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
 #pragma unroll
   for (int q = 0; q < W; ++q) nspl[q] = s_nsplit[q * 32 + lane];
 
-  for (unsigned long long item = gwarp; item < p.total_items; item += nwarps) {
+  for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
     const unsigned long long local = item - blk.item_off;
@@ -468,6 +498,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
   __syncthreads();
 
   const uint32_t lane = lane_id();
+  const uint32_t lanebit = 1u << lane;
   const TransposeLane tr(lane);
   // split masks: bit of the uniform operand that enables split k of word q*32+lane
   uint32_t mlo[W][MAXK], mhi[W][MAXK];
@@ -487,7 +518,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
 
-  for (unsigned long long item = gwarp; item < p.total_items; item += nwarps) {
+  for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
     const unsigned long long local = item - blk.item_off;
@@ -500,7 +531,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
     const unsigned long long nslabs = (ns + 31) / 32;
     const unsigned long long s0 = st * blk.ts, s1 = min(s0 + blk.ts, nslabs);
     const unsigned long long cand_off = blk.cand_off, nb = blk.nb;
+    const uint32_t nu_item = (uint32_t)(u1 - u0);  // <= 64 (kTileU)
     uint32_t evaluated = 0;
+    // the item's uniform operands, lane l holds u0 + l and u0 + 32 + l; broadcast by shuffle
+    uint32_t xa[W], xb[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) { xa[q] = 0; xb[q] = 0; }
+    if (lane < nu_item) load_cs<W>(ubase, u0 + lane, xa);
+    if (lane + 32 < nu_item) load_cs<W>(ubase, u0 + 32 + lane, xb);
 
     for (unsigned long long s = s0; s < s1; ++s) {
       uint32_t T[W];
@@ -525,35 +563,44 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
       const unsigned long long sj = s * 32 + lane;
       const bool lane_ok = sj < ns;
 
-      for (unsigned long long u = u0; u < u1; u += G) {
+      // one batch of G groups; FULL batches need no per-group bounds test
+      auto batch = [&](uint32_t ub, auto full_tag) {
+        constexpr bool FULL = decltype(full_tag)::value;
         uint32_t cs[G][W];
         bool valid[G], skip[G];
+        uint32_t xs[W];  // G divides 32: a batch never straddles the two halves
+#pragma unroll
+        for (int q = 0; q < W; ++q) xs[q] = ub >= 32 ? xb[q] : xa[q];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const bool active = u + g < u1;
+          const uint32_t ui = ub + g;
           uint32_t x[W];
 #pragma unroll
-          for (int q = 0; q < W; ++q) x[q] = 0;
-          if (active) load_cs<W>(ubase, u + g, x);
+          for (int q = 0; q < W; ++q) x[q] = __shfl_sync(kFull, xs[q], ui & 31);
+          uint32_t acc[W];
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            uint32_t acc = ((x[0] & 1u) ? T[q] : 0u) | (((x[q] >> lane) & 1u) ? Teps : 0u);
+            acc[q] = ((x[0] & 1u) ? T[q] : 0u) | ((x[q] & lanebit) ? Teps : 0u);
 #pragma unroll
             for (int k = 0; k < MAXK; ++k) {
               const uint32_t hit = (x[0] & mlo[q][k]) | (W == 2 ? (x[W - 1] & mhi[q][k]) : 0u);
-              acc |= hit ? tk[q][k] : 0u;
+              acc[q] |= hit ? tk[q][k] : 0u;
             }
-            cs[g][q] = tr(acc);
           }
-          valid[g] = active && lane_ok;
+#pragma unroll
+          for (int q = 0; q < W; ++q) cs[g][q] = tr(acc[q]);
+          valid[g] = FULL ? lane_ok : (lane_ok && ui < nu_item);
           skip[g] = cs_equal<W>(cs[g], x);
-          evaluated += valid[g] ? 1u : 0u;
         }
+        evaluated += lane_ok ? min((uint32_t)G, nu_item - ub) : 0u;
         process_batch<W, G>(p, cs, valid, skip, [&](int g) {
-          const unsigned long long ui = u + g;
+          const unsigned long long ui = u0 + ub + g;
           return cand_off + (SLICE_A ? sj * nb + ui : ui * nb + sj);
         });
-      }
+      };
+      uint32_t ub = 0;
+      for (; ub + G <= nu_item; ub += G) batch(ub, std::true_type{});
+      if (ub < nu_item) batch(ub, std::false_type{});
     }
     const uint32_t tot = __reduce_add_sync(kFull, evaluated);
     if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
@@ -574,7 +621,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
   constexpr int G = Batch<W>::G;
 
-  for (unsigned long long item = gwarp; item < p.total_items; item += nwarps) {
+  for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
     const unsigned long long local = item - blk.item_off;
@@ -590,7 +637,17 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
     unsigned long long s0 = st * blk.ts;
     const unsigned long long s1 = min(s0 + blk.ts, nslabs);
     if (tri) s0 = max(s0, (u0 + 1) / 32);  // slabs entirely at or below the diagonal hold no j > i
+    const uint32_t nu_item = (uint32_t)(u1 - u0);  // <= 64 (kTileU)
     uint32_t evaluated = 0;
+    const unsigned long long cand_off = blk.cand_off, na = blk.na, nb = blk.nb;
+    // narrow CSs: the item's uniform operands are held by the lanes and broadcast by shuffle
+    uint32_t xa[W], xb[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) { xa[q] = 0; xb[q] = 0; }
+    if (W <= 2) {
+      if (lane < nu_item) load_cs<W>(p.arena, u_base + u0 + lane, xa);
+      if (lane + 32 < nu_item) load_cs<W>(p.arena, u_base + u0 + 32 + lane, xb);
+    }
 
     for (unsigned long long s = s0; s < s1; ++s) {
       const unsigned long long sj = s * 32 + lane;
@@ -601,29 +658,35 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
 #pragma unroll
         for (int q = 0; q < W; ++q) y[q] = 0;
       }
-      for (unsigned long long u = u0; u < u1; u += G) {
-        if (tri && u >= s * 32 + 31) break;  // no j > i left in this slab
+      for (uint32_t ub = 0; ub < nu_item; ub += G) {
+        if (tri && u0 + ub >= s * 32 + 31) break;  // no j > i left in this slab
         uint32_t cs[G][W];
         bool valid[G], skip[G];
+        const bool hi_half = ub >= 32;
+        uint32_t nvalid = 0;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const unsigned long long ui = u + g;
-          bool active = ui < u1;
+          const uint32_t ui = ub + g;
+          const bool active = ui < nu_item;
           uint32_t x[W];
-          if (active) load_cs<W>(p.arena, u_base + ui, x);
-          else {
+          if (W <= 2) {
+#pragma unroll
+            for (int q = 0; q < W; ++q) x[q] = __shfl_sync(kFull, hi_half ? xb[q] : xa[q], ui & 31);
+          } else if (active) {
+            load_cs<W>(p.arena, u_base + u0 + ui, x);
+          } else {
 #pragma unroll
             for (int q = 0; q < W; ++q) x[q] = 0;
           }
 #pragma unroll
           for (int q = 0; q < W; ++q) cs[g][q] = x[q] | y[q];
-          valid[g] = active && lane_ok && (!tri || sj > ui);
+          valid[g] = active && lane_ok && (!tri || sj > u0 + ui);
           skip[g] = cs_equal<W>(cs[g], x) || cs_equal<W>(cs[g], y);
-          evaluated += valid[g] ? 1u : 0u;
+          nvalid += valid[g] ? 1u : 0u;
         }
-        const unsigned long long cand_off = blk.cand_off, na = blk.na, nb = blk.nb;
+        evaluated += nvalid;
         process_batch<W, G>(p, cs, valid, skip, [&](int g) {
-          const unsigned long long ui = u + g;
+          const unsigned long long ui = u0 + ub + g;
           const unsigned long long i = slice_a ? sj : ui;
           const unsigned long long j = slice_a ? ui : sj;
           return cand_off + (tri ? i * na - i * (i + 1) / 2 + (j - i - 1) : i * nb + j);
@@ -674,7 +737,9 @@ __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long
   for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p.nsplit[i];
   __syncthreads();
   const unsigned long long total = n_q + n_s;
-  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+  const unsigned long long tb = p.item_begin;  // this rank's share [tb, te)
+  const unsigned long long te = total < (unsigned long long)p.total_items ? total : (unsigned long long)p.total_items;
+  for (unsigned long long t = tb + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < te;
        t += (unsigned long long)gridDim.x * blockDim.x) {
     uint32_t x[W], cs[1][W];
     bool valid[1] = {true}, skip[1];
@@ -694,7 +759,7 @@ __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long
     process_batch<W, 1>(p, cs, valid, skip, [&](int) { return rank[0]; });
   }
   __syncthreads();
-  if (threadIdx.x == 0 && blockIdx.x == 0) atomicAdd(&p.ctl->evaluated, total);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && te > tb) atomicAdd(&p.ctl->evaluated, te - tb);
 }
 
 // Seeds (Alg. 1 line 3): one thread, symbols in Sigma order (deterministic).
@@ -735,10 +800,11 @@ __global__ void k_transpose(const uint32_t* __restrict__ arena, unsigned long lo
   }
 }
 
-// Rebuild the dedup set from the first `count` arena entries (after growth).
+// (Re)insert arena entries [base, base + count) into the dedup set (after growth, or
+// after a multi-rank level merge; inserting a present key is a no-op).
 template <int W>
-__global__ void k_rehash(LevelParams p, unsigned long long count) {
-  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+__global__ void k_rehash(LevelParams p, unsigned long long base, unsigned long long count) {
+  for (unsigned long long t = base + (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; t < base + count;
        t += (unsigned long long)gridDim.x * blockDim.x) {
     uint32_t x[W];
     load_cs<W>(p.arena, t, x);
@@ -837,7 +903,7 @@ int launch_concat_fast_t(const LevelParams& p, cudaStream_t st) {
   const size_t smem = p.nblocks * sizeof(Block) + (size_t)MAXK * 32 * W * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items);
+  const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
   k_concat_fast<W, MAXK, SA><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
@@ -858,7 +924,7 @@ int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
   }
   const size_t smem = pair_smem(p, W);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_concat<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = grid_for(k_concat<W>, kWarps * 32, smem, kWarps, p.total_items);
+  const int grid = grid_for(k_concat<W>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
   k_concat<W><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
@@ -867,7 +933,7 @@ template <int W>
 int launch_union_t(const LevelParams& p, cudaStream_t st) {
   const size_t smem = p.nblocks * sizeof(Block);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_union<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = grid_for(k_union<W>, kWarps * 32, smem, kWarps, p.total_items);
+  const int grid = grid_for(k_union<W>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
   k_union<W><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
@@ -929,9 +995,9 @@ int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t cou
                  return 1);
 }
 
-int launch_rehash(int W32, const LevelParams& p, uint64_t count, cudaStream_t st) {
+int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, cudaStream_t st) {
   const int grid = (int)std::min<unsigned long long>((count + 255) / 256, (unsigned long long)sm_count() * 8);
-  REI_DISPATCH_W(W32, k_rehash<W><<<std::max(grid, 1), 256, 0, st>>>(p, count); return 1);
+  REI_DISPATCH_W(W32, k_rehash<W><<<std::max(grid, 1), 256, 0, st>>>(p, base, count); return 1);
 }
 
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,

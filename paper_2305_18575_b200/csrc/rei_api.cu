@@ -9,6 +9,8 @@
 // launches the level kernels (levels.cu) and reads back one 64-byte control line.
 // The language cache, dedup set and transposed slabs never leave the device.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -22,6 +24,44 @@
 #include "../../include/rei.h"
 #include "rei_common.cuh"
 #include "rei_host.h"
+
+namespace rei {
+namespace {
+// NCCL is resolved at run time (dlopen), only when a multi-GPU context is made:
+// the library itself does not depend on libnccl, so loading it can never shadow the
+// NCCL build torch ships (callers import torch first, then its libnccl is reused).
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+};
+
+NcclApi& nccl_api() {
+  static NcclApi a;
+  static bool tried = false;
+  if (tried) return a;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) return a;
+  a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+  a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+  a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+  a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+  a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(h, "ncclBroadcast"));
+  a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+  a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast && a.GroupStart &&
+         a.GroupEnd;
+  return a;
+}
+}  // namespace
+}  // namespace rei
 
 namespace rei {
 namespace {
@@ -90,6 +130,15 @@ struct Ctx {
   std::string err;
   rei_result result{};
 
+  // multi-rank
+  int world = 1, rank = 0;
+  void* nccl = nullptr;              // ncclComm_t (one process per GPU)
+  LevelCtl* d_ctl_all = nullptr;     // [world] gathered control lines
+  uint32_t* g_cs = nullptr;          // gathered new-CS lists of a level
+  unsigned long long* g_bp = nullptr;
+  uint64_t gather_cap = 0;
+  MergeScratch merge;
+
   // profiling
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
   uint64_t launches = 0;
@@ -107,6 +156,9 @@ struct Ctx {
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_blocks) cudaFreeHost(h_blocks);
     for (auto e : ev_pool) cudaEventDestroy(e);
+    cudaFree(d_ctl_all); cudaFree(g_cs); cudaFree(g_bp);
+    free_merge_scratch(merge);
+    if (nccl) nccl_api().CommDestroy((ncclComm_t)nccl);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -446,7 +498,7 @@ rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
   fill_params(c, p);
   EventPair ep;
   c->begin_kernel(REI_K_OTHER, ep);
-  int n = launch_rehash(c->W32, p, entries, c->stream);
+  int n = launch_rehash(c->W32, p, 0, entries, c->stream);
   c->end_kernel(ep, n);
   CUDA_OK(c, cudaGetLastError());
   return REI_OK;
@@ -476,9 +528,17 @@ rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
   return REI_OK;
 }
 
-rei_status solve_impl(Ctx* c, uint32_t max_cost) {
-  const rei_costs& k = c->costs;
-  const int c1 = (int)k.sym;
+// Multi-rank transport of the sharded level.  `m` holds the ranks
+// driven by this process: all `world` ranks (virtual ranks, rei_solve_group) or
+// exactly one (one process per GPU; the exchange goes through NCCL).
+struct Comm {
+  int world = 1;
+  int rank0 = 0;
+  std::vector<Ctx*> m;
+  void* nccl = nullptr;  // ncclComm_t of m[0] when each process holds one rank
+};
+
+void reset_search(Ctx* c) {
   c->levels.clear();
   c->stats.clear();
   c->regex.clear();
@@ -487,31 +547,207 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
   memset(&c->result, 0, sizeof(c->result));
   c->result.n_ic = (uint32_t)c->tab.n;
   c->result.cs_words = (uint32_t)c->W32;
+}
+
+// Every rank's control line, in rank order, on every member.
+rei_status gather_ctl(Comm& g, std::vector<LevelCtl>& all) {
+  all.assign(g.world, LevelCtl{});
+  if (!g.nccl) {
+    for (size_t i = 0; i < g.m.size(); ++i) all[g.rank0 + i] = *g.m[i]->h_ctl;
+    return REI_OK;
+  }
+  Ctx* c = g.m[0];
+  if (nccl_api().AllGather(c->ctl, c->d_ctl_all, sizeof(LevelCtl), ncclUint8, (ncclComm_t)g.nccl, c->stream) !=
+      ncclSuccess) {
+    c->err = "ncclAllGather(level control) failed";
+    return REI_ENCCL;
+  }
+  CUDA_OK(c, cudaMemcpyAsync(all.data(), c->d_ctl_all, sizeof(LevelCtl) * g.world, cudaMemcpyDeviceToHost,
+                             c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->d2h_bytes += sizeof(LevelCtl) * g.world;
+  return REI_OK;
+}
+
+rei_status ensure_gather(Ctx* c, uint64_t m) {
+  if (c->gather_cap >= m) return REI_OK;
+  cudaFree(c->g_cs);
+  cudaFree(c->g_bp);
+  c->g_cs = nullptr;
+  c->g_bp = nullptr;
+  const uint64_t cap = std::max<uint64_t>(m, 2 * c->gather_cap);
+  CUDA_OK(c, cudaMalloc(&c->g_cs, cap * 4ull * c->W32));
+  CUDA_OK(c, cudaMalloc(&c->g_bp, cap * 8ull));
+  c->gather_cap = cap;
+  return REI_OK;
+}
+
+// All-gather the ranks' new-CS lists of the level (in rank order) and replace each
+// member's level with the canonical first-occurrence merge.  Returns its size.
+rei_status exchange_level(Comm& g, uint64_t begin, const std::vector<LevelCtl>& all, uint64_t* out_count) {
+  std::vector<uint64_t> off(g.world + 1, 0);
+  for (int r = 0; r < g.world; ++r) off[r + 1] = off[r] + all[r].count;
+  const uint64_t M = off[g.world];
+  uint64_t canon = ~0ull;
+  // 1) gather every rank's list into every member (all gathers complete before any
+  //    member overwrites its level with the merge: the lists are read in place)
+  for (size_t i = 0; i < g.m.size(); ++i) {
+    Ctx* c = g.m[i];
+    rei_status s = ensure_gather(c, M);
+    if (s != REI_OK) return s;
+    const size_t csb = 4ull * c->W32;
+    if (!g.nccl) {
+      for (int r = 0; r < g.world; ++r) {
+        Ctx* src = g.m[r - g.rank0];
+        if (!all[r].count) continue;
+        CUDA_OK(c, cudaMemcpyPeerAsync(c->g_cs + off[r] * c->W32, c->device, src->arena + begin * c->W32,
+                                       src->device, all[r].count * csb, c->stream));
+        CUDA_OK(c, cudaMemcpyPeerAsync(c->g_bp + off[r], c->device, src->bp + begin, src->device,
+                                       all[r].count * 8ull, c->stream));
+      }
+    } else {
+      const int me = g.rank0;
+      nccl_api().GroupStart();
+      for (int r = 0; r < g.world; ++r) {
+        if (!all[r].count) continue;
+        nccl_api().Broadcast(r == me ? (const void*)(c->arena + begin * c->W32) : nullptr, c->g_cs + off[r] * c->W32,
+                      all[r].count * c->W32, ncclUint32, r, (ncclComm_t)g.nccl, c->stream);
+        nccl_api().Broadcast(r == me ? (const void*)(c->bp + begin) : nullptr, c->g_bp + off[r], all[r].count,
+                      ncclUint64, r, (ncclComm_t)g.nccl, c->stream);
+      }
+      if (nccl_api().GroupEnd() != ncclSuccess) {
+        c->err = "NCCL all-gather of the level lists failed";
+        return REI_ENCCL;
+      }
+    }
+  }
+  for (Ctx* c : g.m) CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  // 2) canonical merge on every member (identical input bytes -> identical output)
+  for (Ctx* c : g.m) {
+    uint64_t cnt = 0;
+    std::string err;
+    if (!merge_level(c->W32, c->g_cs, c->g_bp, M, c->arena + begin * c->W32, c->bp + begin, &cnt, c->merge,
+                     c->stream, err, &c->launches)) {
+      c->err = err;
+      return REI_ECUDA;
+    }
+    if (canon != ~0ull && canon != cnt) {
+      g.m[0]->err = c->err = "ranks disagree on the merged level size";
+      return REI_ECUDA;
+    }
+    canon = cnt;
+    // the dedup set must hold every rank's new CSs (present keys are no-ops)
+    LevelParams p;
+    fill_params(c, p);
+    EventPair ep;
+    c->begin_kernel(REI_K_OTHER, ep);
+    int n = launch_rehash(c->W32, p, begin, cnt, c->stream);
+    c->end_kernel(ep, n);
+    CUDA_OK(c, cudaGetLastError());
+  }
+  *out_count = canon == ~0ull ? 0 : canon;
+  return REI_OK;
+}
+
+rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, uint64_t nq, uint64_t ns,
+                        const std::vector<Block>& cat, const std::vector<Block>& uni) {
+  const rei_costs& k = c->costs;
+  rei_status s;
+  LevelParams p;
+  fill_params(c, p);
+  p.out_base = begin;
+  if ((s = reset_ctl(c)) != REI_OK) return s;
+  // operand blocks -> device (one small H2D per level).  Concatenation blocks are
+  // split by orientation (left or right operand sliced): one launch each.
+  std::vector<Block> catv[2];
+  for (const Block& b : cat) catv[b.slice_a ? 1 : 0].push_back(b);
+  for (auto& v : catv) renumber_items(v);
+  const std::vector<Block>* lists[3] = {&catv[0], &catv[1], &uni};
+  for (int r = 0; r < 3; ++r) {
+    if (lists[r]->empty()) continue;
+    std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
+    CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, c->h_blocks + r * Ctx::kMaxBlocks,
+                               lists[r]->size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += lists[r]->size() * sizeof(Block);
+  }
+  // this rank's share of every work list (SURVEY 8(e) partition)
+  auto share = [&](uint64_t total, LevelParams& q) {
+    uint64_t b = 0, e = total;
+    rei_partition(total, world, rank, &b, &e);
+    q.item_begin = b;
+    q.total_items = e;
+    return e > b;
+  };
+  if (nq + ns) {
+    const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
+    const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
+    LevelParams pq = p;
+    if (share(nq + ns, pq)) {
+      EventPair ep;
+      c->begin_kernel(REI_K_UNARY, ep);
+      int n = launch_unary(c->W32, pq, nq, ns, bq, bs, nq, c->stream);
+      c->end_kernel(ep, n);
+    }
+  }
+  for (int r = 0; r < 2; ++r) {
+    if (catv[r].empty()) continue;
+    LevelParams pc = p;
+    pc.blocks = c->d_blocks + r * Ctx::kMaxBlocks;
+    pc.nblocks = (uint32_t)catv[r].size();
+    if (!share(items_of(catv[r]), pc)) continue;
+    EventPair ep;
+    c->begin_kernel(REI_K_CONCAT, ep);
+    int n = launch_concat(c->W32, pc, r == 1, c->stream);
+    c->end_kernel(ep, n);
+  }
+  if (!uni.empty()) {
+    LevelParams pu = p;
+    pu.blocks = c->d_blocks + 2 * Ctx::kMaxBlocks;
+    pu.nblocks = (uint32_t)uni.size();
+    if (share(items_of(uni), pu)) {
+      EventPair ep;
+      c->begin_kernel(REI_K_UNION, ep);
+      int n = launch_union(c->W32, pu, c->stream);
+      c->end_kernel(ep, n);
+    }
+  }
+  CUDA_OK(c, cudaGetLastError());
+  return REI_OK;
+}
+
+// Algorithm 1 over all ranks of `g` (world = 1: the single-GPU path, no exchange).
+rei_status solve_group(Comm& g, uint32_t max_cost) {
+  Ctx* c0 = g.m[0];
+  const rei_costs& k = c0->costs;
+  const int c1 = (int)k.sym;
+  const bool multi = g.world > 1;
+  rei_status s;
+  for (Ctx* c : g.m) reset_search(c);
   uint64_t cand = 1;  // Alg. 1 line 1: the empty regex is the first candidate (A9)
 
-  const uint64_t total_ex = c->P.size() + c->N.size();
-  const bool empty_ok = c->P.empty() ||
-                        (c->err_num && (uint64_t)c->P.size() * c->err_den <= (uint64_t)c->err_num * total_ex);
-  if (empty_ok) {
-    c->regex = "empty";
-    c->result.cost = k.sym;
-    c->result.candidates = cand;
+  const uint64_t total_ex = c0->P.size() + c0->N.size();
+  const bool empty_ok = c0->P.empty() ||
+                        (c0->err_num && (uint64_t)c0->P.size() * c0->err_den <= (uint64_t)c0->err_num * total_ex);
+  const bool eps_ok = c0->P.size() == 1 && c0->P[0].empty();  // Alg. 1 line 2
+  if (empty_ok || eps_ok) {
+    for (Ctx* c : g.m) {
+      c->regex = empty_ok ? "empty" : "eps";
+      c->result.cost = k.sym;
+      c->result.candidates = cand;
+    }
     return REI_OK;
   }
-  if (c->P.size() == 1 && c->P[0].empty()) {  // Alg. 1 line 2
-    c->regex = "eps";
-    c->result.cost = k.sym;
-    c->result.candidates = cand;
-    return REI_OK;
+  if (multi && c0->W32 > 2) {
+    c0->err = "the multi-rank level exchange supports |IC| <= 64";
+    return REI_EINVAL;
   }
-  rei_status s = clear_dedup(c);
-  if (s != REI_OK) return s;
 
-  // ---- level c1: the alphabet symbols (Alg. 1 line 3)
-  {
+  // ---- level c1: the alphabet symbols (Alg. 1 line 3), identical on every rank
+  uint64_t found_seed = ~0ull;
+  for (Ctx* c : g.m) {
+    if ((s = clear_dedup(c)) != REI_OK) return s;
     LevelInfo lv;
     lv.cost = c1;
-    lv.begin = 0;
     lv.seeds = true;
     LevelParams p;
     fill_params(c, p);
@@ -526,155 +762,150 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
     double ms;
     c->collect_events(&ms);
     lv.size = c->h_ctl->count;
-    cand += c->alphabet.size();
     c->levels[c1] = lv;
     c->arena_used = lv.size;
     rei_level_stat st{};
     st.cost = c1;
     st.unique = lv.size;
     st.ms = ms;
-    if (c->h_ctl->found_rank != ~0ull) {
-      const uint64_t r = c->h_ctl->found_rank;
-      cand = 1 + r + 1;
-      st.complete = 0;
-      c->stats.push_back(st);
-      c->result.candidates = cand;
-      return finish_found(c, c1, r);
-    }
-    st.complete = 1;
+    found_seed = c->h_ctl->found_rank;
+    st.complete = found_seed == ~0ull ? 1 : 0;
     c->stats.push_back(st);
-    c->levels[c1].slab = 0;
+  }
+  if (found_seed != ~0ull) {
+    for (Ctx* c : g.m) {
+      c->result.candidates = 1 + found_seed + 1;
+      if ((s = finish_found(c, c1, found_seed)) != REI_OK) return s;
+    }
+    return REI_OK;
+  }
+  cand += c0->alphabet.size();
+  for (Ctx* c : g.m) {
     EventPair et;
     c->begin_kernel(REI_K_TRANSPOSE, et);
-    n = launch_transpose(c->W32, c->arena, 0, lv.size, c->tarena, 0, c->stream);
+    int n = launch_transpose(c->W32, c->arena, 0, c->arena_used, c->tarena, 0, c->stream);
     c->end_kernel(et, n);
-    c->slabs_used = (lv.size + 31) / 32;
+    c->slabs_used = (c->arena_used + 31) / 32;
     c->result.last_complete_cost = c1;
     c->result.cand_complete = cand;
   }
 
   std::vector<Block> cat, uni;
+  std::vector<LevelCtl> all;
   for (int cost = c1 + 1; cost <= (int)max_cost; ++cost) {
     LevelInfo lv;
     lv.cost = cost;
     uint64_t nq, ns, ncat, nuni;
-    plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);
+    plan_level(c0, cost, lv, cat, uni, nq, ns, ncat, nuni);  // identical on every rank
     if (lv.plan.empty()) continue;
     if ((int)(cat.size() + uni.size()) > Ctx::kMaxBlocks) {
-      c->err = "too many operand blocks in one level";
+      c0->err = "too many operand blocks in one level";
       return REI_EINVAL;
     }
     // grow ahead of the level when its new CSs may not fit (a level rarely has more
-    // than ~4x the previous level's new CSs; an overflow still triggers a retry)
-    {
-      const uint64_t prev = c->stats.empty() ? 0 : c->stats.back().unique;
-      const uint64_t expect = std::min<uint64_t>(nq + ns + ncat + nuni, 4 * prev + 1024);
+    // than ~4x the previous level's new CSs; an overflow still triggers a retry).  In
+    // multi-rank mode a rank also stages its own list there, hence the factor 2.
+    const uint64_t prev = c0->stats.empty() ? 0 : c0->stats.back().unique;
+    const uint64_t expect = std::min<uint64_t>(nq + ns + ncat + nuni, (multi ? 8 : 4) * prev + 1024);
+    for (Ctx* c : g.m) {
       if (c->arena_used + expect > c->cap || c->slabs_used + expect / 32 + 2 > c->slab_cap) {
         if ((s = grow(c, c->arena_used + expect)) != REI_OK && s != REI_OUT_OF_MEMORY) return s;
       }
     }
-    lv.begin = c->arena_used;
-    lv.slab = c->slabs_used;
+    lv.begin = c0->arena_used;
+    lv.slab = c0->slabs_used;
     rei_level_stat st{};
     st.cost = (uint32_t)cost;
     st.cand_q = nq; st.cand_s = ns; st.cand_c = ncat; st.cand_u = nuni;
     double level_ms = 0;
     for (int attempt = 0;; ++attempt) {
-      LevelParams p;
-      fill_params(c, p);
-      p.out_base = lv.begin;
-      if ((s = reset_ctl(c)) != REI_OK) return s;
-      // operand blocks -> device (one small H2D per level).  Concatenation blocks are
-      // split by orientation (left or right operand sliced): one launch each.
-      std::vector<Block> catv[2];
-      for (const Block& b : cat) catv[b.slice_a ? 1 : 0].push_back(b);
-      for (auto& v : catv) renumber_items(v);
-      const std::vector<Block>* lists[3] = {&catv[0], &catv[1], &uni};
-      for (int r = 0; r < 3; ++r) {
-        if (lists[r]->empty()) continue;
-        std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
-        CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, c->h_blocks + r * Ctx::kMaxBlocks,
-                                   lists[r]->size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
-        c->h2d_bytes += lists[r]->size() * sizeof(Block);
+      for (size_t i = 0; i < g.m.size(); ++i)
+        if ((s = launch_level(g.m[i], g.rank0 + (int)i, g.world, cost, lv.begin, nq, ns, cat, uni)) != REI_OK)
+          return s;
+      for (Ctx* c : g.m) {
+        if ((s = read_ctl(c)) != REI_OK) return s;
+        double ms;
+        c->collect_events(&ms);
+        if (c == c0) level_ms += ms;
       }
-      if (nq + ns) {
-        const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
-        const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
-        EventPair ep;
-        c->begin_kernel(REI_K_UNARY, ep);
-        int n = launch_unary(c->W32, p, nq, ns, bq, bs, nq, c->stream);
-        c->end_kernel(ep, n);
+      if ((s = gather_ctl(g, all)) != REI_OK) return s;
+      bool overflow = false;
+      uint64_t need = 0;
+      for (auto& l : all) {
+        overflow |= l.overflow != 0;
+        need = std::max<uint64_t>(need, lv.begin + l.count + 1);
       }
-      for (int r = 0; r < 2; ++r) {
-        if (catv[r].empty()) continue;
-        LevelParams pc = p;
-        pc.blocks = c->d_blocks + r * Ctx::kMaxBlocks;
-        pc.nblocks = (uint32_t)catv[r].size();
-        pc.total_items = items_of(catv[r]);
-        EventPair ep;
-        c->begin_kernel(REI_K_CONCAT, ep);
-        int n = launch_concat(c->W32, pc, r == 1, c->stream);
-        c->end_kernel(ep, n);
-      }
-      if (!uni.empty()) {
-        LevelParams pu = p;
-        pu.blocks = c->d_blocks + 2 * Ctx::kMaxBlocks;
-        pu.nblocks = (uint32_t)uni.size();
-        pu.total_items = items_of(uni);
-        EventPair ep;
-        c->begin_kernel(REI_K_UNION, ep);
-        int n = launch_union(c->W32, pu, c->stream);
-        c->end_kernel(ep, n);
-      }
-      CUDA_OK(c, cudaGetLastError());
-      if ((s = read_ctl(c)) != REI_OK) return s;
-      double ms;
-      c->collect_events(&ms);
-      level_ms += ms;
-      if (!c->h_ctl->overflow) break;
+      if (!overflow) break;
       // capacity exceeded: grow the cache / dedup set and redo the level
-      const uint64_t need = lv.begin + c->h_ctl->count + 1;
-      s = grow(c, need);
-      if (s != REI_OK) {
-        c->result.candidates = c->result.cand_complete;
-        return s;
+      for (Ctx* c : g.m) {
+        if ((s = grow(c, need)) != REI_OK) {
+          for (Ctx* d : g.m) d->result.candidates = d->result.cand_complete;
+          return s;
+        }
       }
     }
-    lv.size = c->h_ctl->count;
-    c->arena_used = lv.begin + lv.size;
-    st.unique = lv.size;
+    uint64_t found_rank = ~0ull, evaluated = 0, eval_c = 0, eval_u = 0;
+    for (auto& l : all) {
+      found_rank = std::min<uint64_t>(found_rank, l.found_rank);
+      evaluated += l.evaluated;
+      eval_c += l.eval_c;
+      eval_u += l.eval_u;
+    }
+    const bool found = found_rank != ~0ull;
+    const bool complete = !found || (c0->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
+    uint64_t size = all[g.rank0].count;
+    if (multi && complete) {
+      if ((s = exchange_level(g, lv.begin, all, &size)) != REI_OK) return s;
+    }
+    lv.size = size;
+    st.unique = size;
     st.ms = level_ms;
-    const bool found = c->h_ctl->found_rank != ~0ull;
-    const bool complete = !found || (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
     st.complete = complete ? 1 : 0;
-    st.evaluated = complete ? (nq + ns + ncat + nuni) : c->h_ctl->evaluated;
-    st.eval_c = complete ? ncat : c->h_ctl->eval_c;
-    st.eval_u = complete ? nuni : c->h_ctl->eval_u;
-    c->levels[cost] = lv;
-    c->stats.push_back(st);
+    st.evaluated = complete ? (nq + ns + ncat + nuni) : evaluated;
+    st.eval_c = complete ? ncat : eval_c;
+    st.eval_u = complete ? nuni : eval_u;
+    for (Ctx* c : g.m) {
+      c->arena_used = lv.begin + lv.size;
+      c->levels[cost] = lv;
+      c->stats.push_back(st);
+    }
     if (found) {
-      c->result.candidates = cand + st.evaluated;
-      if (complete) {
-        c->result.last_complete_cost = (uint32_t)cost;
-        c->result.cand_complete = cand + st.evaluated;
+      for (Ctx* c : g.m) {
+        c->result.candidates = cand + st.evaluated;
+        if (complete) {
+          c->result.last_complete_cost = (uint32_t)cost;
+          c->result.cand_complete = cand + st.evaluated;
+        }
+        if ((s = finish_found(c, cost, found_rank)) != REI_OK) return s;
       }
-      return finish_found(c, cost, c->h_ctl->found_rank);
+      return REI_OK;
     }
     cand += nq + ns + ncat + nuni;
-    c->result.cand_complete = cand;
-    c->result.candidates = cand;
-    c->result.last_complete_cost = (uint32_t)cost;
-    // transposed copy of level c (the sliced-operand layout for later levels)
-    if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
-      if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
+    for (Ctx* c : g.m) {
+      c->result.cand_complete = cand;
+      c->result.candidates = cand;
+      c->result.last_complete_cost = (uint32_t)cost;
+      // transposed copy of level c (the sliced-operand layout for later levels)
+      if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
+        if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
+      }
+      EventPair et;
+      c->begin_kernel(REI_K_TRANSPOSE, et);
+      int n = launch_transpose(c->W32, c->arena, lv.begin, lv.size, c->tarena, lv.slab, c->stream);
+      c->end_kernel(et, n);
+      c->slabs_used += (lv.size + 31) / 32;
     }
-    EventPair et;
-    c->begin_kernel(REI_K_TRANSPOSE, et);
-    int n = launch_transpose(c->W32, c->arena, lv.begin, lv.size, c->tarena, lv.slab, c->stream);
-    c->end_kernel(et, n);
-    c->slabs_used += (lv.size + 31) / 32;
   }
   return REI_NOT_FOUND;
+}
+
+rei_status solve_impl(Ctx* c, uint32_t max_cost) {
+  Comm g;
+  g.m = {c};
+  g.world = c->world > 1 ? c->world : 1;
+  g.rank0 = c->world > 1 ? c->rank : 0;
+  g.nccl = c->nccl;
+  return solve_group(g, max_cost);
 }
 
 }  // namespace
@@ -742,7 +973,14 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     c->err_den = opts->err_den ? opts->err_den : 1;
     c->flags = opts->flags;
     c->budget = opts->mem_budget_bytes;
-    if (opts->world_size > 1) { g_init_error = "multi-GPU contexts: use rei_init_mgpu"; return REI_EINVAL; }
+    if (opts->world_size > 1) {
+      if (!opts->nccl_unique_id || opts->rank < 0 || opts->rank >= opts->world_size) {
+        g_init_error = "multi-GPU context needs rank in [0, world_size) and an ncclUniqueId";
+        return REI_EINVAL;
+      }
+      c->world = opts->world_size;
+      c->rank = opts->rank;
+    }
   }
   if (opts && opts->device >= 0) {
     if (cudaSetDevice(opts->device) != cudaSuccess) { g_init_error = "cudaSetDevice failed"; return REI_ECUDA; }
@@ -771,6 +1009,18 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       cudaMallocHost(&c->h_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess)
     return fail(std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError()));
   cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
+  if (c->world > 1) {  // one process per GPU: the level exchange runs over NCCL (collective)
+    ncclUniqueId id;
+    memcpy(&id, opts->nccl_unique_id, sizeof(id));
+    ncclComm_t comm;
+    if (!nccl_api().ok || nccl_api().CommInitRank(&comm, c->world, id, c->rank) != ncclSuccess) {
+      g_init_error = "ncclCommInitRank failed";
+      return REI_ENCCL;
+    }
+    c->nccl = comm;
+    if (cudaMalloc(&c->d_ctl_all, sizeof(LevelCtl) * c->world) != cudaSuccess)
+      return fail("device allocation failed (control lines)");
+  }
   if (c->P.empty() && c->N.empty()) {
     // nothing to precompute: only the trivial case P = {} applies
     c->tab.n = 0;
@@ -967,6 +1217,45 @@ rei_status rei_cs_ops(void* ctx, int op, const uint32_t* a, const uint32_t* b, u
   c->collect_events(nullptr);
   cudaFree(da); cudaFree(db); cudaFree(dout);
   return REI_OK;
+}
+
+rei_status rei_nccl_unique_id(void* out, size_t cap) {
+  if (!out || cap < sizeof(ncclUniqueId)) return REI_EINVAL;
+  ncclUniqueId id;
+  if (!rei::nccl_api().ok || rei::nccl_api().GetUniqueId(&id) != ncclSuccess) return REI_ENCCL;
+  memcpy(out, &id, sizeof(id));
+  return REI_OK;
+}
+
+rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_result* out) {
+  if (!ctxs || G < 1) return REI_EINVAL;
+  rei::Comm g;
+  g.world = G;
+  g.rank0 = 0;
+  for (int i = 0; i < G; ++i) {
+    Ctx* c = static_cast<Ctx*>(ctxs[i]);
+    if (!c || c->world > 1) return REI_EINVAL;
+    if (i > 0 && (c->tab.n != g.m[0]->tab.n || c->W32 != g.m[0]->W32 || c->mode != g.m[0]->mode))
+      return REI_EINVAL;
+    c->err.clear();
+    g.m.push_back(c);
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  rei_status s = rei::solve_group(g, max_cost);
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  std::string first_err;
+  for (Ctx* c : g.m)
+    if (first_err.empty()) first_err = c->err;
+  for (Ctx* c : g.m) {
+    c->result.seconds = secs;
+    c->result.regex = c->regex.c_str();
+    uint64_t uniq = 0;
+    for (auto& st : c->stats) uniq += st.unique;
+    c->result.unique = uniq;
+    if (s != REI_OK && s != REI_NOT_FOUND && s != REI_OUT_OF_MEMORY && c->err.empty()) c->err = first_err;
+  }
+  if (out) *out = g.m[0]->result;
+  return s;
 }
 
 void rei_partition(uint64_t total, int G, int g, uint64_t* begin, uint64_t* end) {

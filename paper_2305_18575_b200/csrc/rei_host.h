@@ -35,7 +35,18 @@ int launch_concat(int W32, const LevelParams& p, bool slice_a, cudaStream_t st);
 int launch_union(int W32, const LevelParams& p, cudaStream_t st);
 int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t count, uint32_t* tarena,
                      uint64_t slab_base, cudaStream_t st);
-int launch_rehash(int W32, const LevelParams& p, uint64_t count, cudaStream_t st);
+int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, cudaStream_t st);
+
+// Canonical first-occurrence merge of an all-gathered level list (exchange.cu).
+struct MergeScratch {
+  void *keys = nullptr, *keys2 = nullptr, *pos = nullptr, *pos2 = nullptr, *flags = nullptr, *scan = nullptr,
+       *temp = nullptr;
+  size_t keys_cap = 0, keys2_cap = 0, pos_cap = 0, pos2_cap = 0, flags_cap = 0, scan_cap = 0, temp_cap = 0;
+};
+bool merge_level(int W32, const uint32_t* g_cs, const unsigned long long* g_bp, uint64_t m, uint32_t* out_cs,
+                 unsigned long long* out_bp, uint64_t* out_count, MergeScratch& s, cudaStream_t st,
+                 std::string& err, uint64_t* launches);
+void free_merge_scratch(MergeScratch& s);
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                uint64_t count, cudaStream_t st);
 

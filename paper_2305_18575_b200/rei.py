@@ -102,6 +102,10 @@ def load_library():
     lib.rei_cs_ops.argtypes = [vp, c.c_int, c.POINTER(c.c_uint32), c.POINTER(c.c_uint32),
                                c.POINTER(c.c_uint32), c.c_size_t]
     lib.rei_partition.argtypes = [c.c_uint64, c.c_int, c.c_int, c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)]
+    lib.rei_nccl_unique_id.restype = c.c_int
+    lib.rei_nccl_unique_id.argtypes = [c.c_void_p, c.c_size_t]
+    lib.rei_solve_group.restype = c.c_int
+    lib.rei_solve_group.argtypes = [c.POINTER(c.c_void_p), c.c_int, c.c_uint32, c.POINTER(_Result)]
     _lib = lib
     return lib
 
@@ -153,11 +157,19 @@ class Solver:
     def __init__(self, alphabet: str, P: Sequence[str], N: Sequence[str],
                  costs: Sequence[int] = (1, 1, 1, 1, 1), device: int = -1, stream=None,
                  mem_budget_bytes: int = 0, error: Optional[Tuple[int, int]] = None,
-                 complete_final_level: bool = False):
+                 complete_final_level: bool = False, world_size: int = 1, rank: int = 0,
+                 nccl_id: Optional[bytes] = None):
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
         opts = _Options()
+        self._nccl_id = None
+        if world_size > 1:
+            if nccl_id is None or len(nccl_id) < 128:
+                raise ValueError("world_size > 1 needs the 128-byte nccl_id from rank 0")
+            import torch  # noqa: F401  -- torch's libnccl is the one the library dlopens
+            self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            opts.nccl_unique_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         opts.device = device
         if stream is not None:
             opts.stream = int(getattr(stream, "cuda_stream", stream))
@@ -167,7 +179,7 @@ class Solver:
         else:
             opts.err_num, opts.err_den = 0, 1
         opts.flags = FLAG_COMPLETE_FINAL_LEVEL if complete_final_level else 0
-        opts.world_size, opts.rank = 1, 0
+        opts.world_size, opts.rank = int(world_size), int(rank)
         costs_c = _Costs(*[int(c) for c in costs])
         self._keep = (_strs(P), _strs(N))
         st = lib.rei_init(ctypes.byref(self._h), alphabet.encode("latin-1"), self._keep[0], len(P),
@@ -329,6 +341,31 @@ def partition(total: int, G: int, g: int) -> Tuple[int, int]:
     b, e = ctypes.c_uint64(), ctypes.c_uint64()
     lib.rei_partition(total, G, g, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
+
+
+def nccl_unique_id() -> bytes:
+    """rank 0's ncclUniqueId (128 bytes) for Solver(..., world_size, rank, nccl_id)."""
+    import torch  # noqa: F401  -- load torch's libnccl first; the library dlopens the same one
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    st = lib.rei_nccl_unique_id(buf, 128)
+    if st != REI_OK:
+        raise ReiError(st, "ncclGetUniqueId failed")
+    return buf.raw
+
+
+def solve_group(solvers: Sequence["Solver"], max_cost: int = 500) -> Result:
+    """Run G single-GPU contexts as ranks 0..G-1 of one sharded search (virtual ranks)."""
+    lib = load_library()
+    arr = (ctypes.c_void_p * len(solvers))(*[s._h.value for s in solvers])
+    r = _Result()
+    st = lib.rei_solve_group(arr, len(solvers), int(max_cost), ctypes.byref(r))
+    if st not in (REI_OK, REI_NOT_FOUND, REI_OUT_OF_MEMORY):
+        raise ReiError(st, solvers[0]._err())
+    s0 = solvers[0]
+    return Result(STATUS_NAMES[st], (r.regex or b"").decode("latin-1"), r.cost, r.last_complete_cost,
+                  r.candidates, r.cand_complete, r.unique, r.seconds, r.n_ic, r.cs_words,
+                  s0.level_stats())
 
 
 def solve(spec, max_cost: int = 500, **kw) -> Result:

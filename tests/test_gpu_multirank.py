@@ -1,0 +1,84 @@
+"""Sharded level with virtual ranks on one GPU (``-m gpu``).
+
+G contexts act as ranks 0..G-1 of one search: each enumerates its share of every
+level, the new-CS lists are all-gathered (device copies instead of NCCL) and
+merged canonically.  Checked against the oracle: same c*, the same set of CSs at
+every level, and every rank holding a byte-identical cache (same order)."""
+import json
+import os
+
+import pytest
+
+import oracle
+import specgen
+from regex_tools import cost as re_cost, parse, precise
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_18575_b200 import build
+    build.build()
+
+
+def group(sp, G, **kw):
+    from paper_2305_18575_b200 import Solver
+    return [Solver.from_spec(sp, device=0, **kw) for _ in range(G)]
+
+
+CASES = [(specgen.C1_TOY, 12), (specgen.E1, 12), (specgen.TABLE1_ROW1, 15),
+         (specgen.gen_type1("01", 4, 5, 5, 3), 20), (specgen.gen_type2("01", 7, 6, 6, 0), 16),
+         (specgen.C1_TOY.with_costs((2, 1, 3, 1, 1)), 20)]
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+@pytest.mark.parametrize("sp,K", CASES, ids=[c[0].name or "rand" for c in CASES])
+def test_virtual_ranks_match_oracle(sp, K, G):
+    from paper_2305_18575_b200 import solve_group
+    o = oracle.Oracle.from_spec(sp)
+    ro = o.solve(K, complete_final_level=True)
+    members = group(sp, G, complete_final_level=True)
+    rg = solve_group(members, K)
+    assert rg.status == ro.status
+    last = ro.cost if ro.status == "found" else K
+    for c in range(1, last + 1):
+        lists = [m.level_cs(c) for m in members]
+        for other in lists[1:]:
+            assert other == lists[0], c          # identical caches, identical order
+        assert sorted(lists[0]) == sorted(o.level_cs(c)), c
+    if ro.status == "found":
+        assert rg.cost == ro.cost
+        assert precise(rg.regex, sp.P, sp.N)
+        assert re_cost(parse(rg.regex), sp.costs) == ro.cost
+        assert all(m.level_stats()[-1].unique == rg.levels[-1].unique for m in members)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_virtual_ranks_early_exit(G):
+    from paper_2305_18575_b200 import solve_group
+    sp = specgen.INTRO
+    ro = oracle.Oracle.from_spec(sp).solve(20)
+    rg = solve_group(group(sp, G), 20)
+    assert rg.status == "found" and rg.cost == ro.cost
+    assert precise(rg.regex, sp.P, sp.N)
+    assert rg.cand_complete == ro.cand_complete
+
+
+def test_virtual_ranks_table1_row1_full():
+    # the bench workload sharded over 2 virtual ranks: c* = 28 and the golden counts
+    from paper_2305_18575_b200 import solve_group
+    sp = specgen.TABLE1_ROW1
+    rg = solve_group(group(sp, 2), 40)
+    assert rg.status == "found" and rg.cost == 28
+    assert precise(rg.regex, sp.P, sp.N)
+    path = os.path.join(GOLDEN, "table1_row1_oracle.json")
+    if os.path.exists(path):
+        want = {l["cost"]: l["unique"] for l in json.load(open(path))["levels"]}
+        for l in rg.levels:
+            if l.cost < 28:
+                assert l.unique == want[l.cost], l.cost
