@@ -10,9 +10,12 @@ hot-path row (Q, S, concat, union, precision test, dedup, append, reconstruction
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) every rank solves the workload independently (replicas;
-"scaling": "weak"); the time is the max over ranks.  ``--impl reference`` times the
-CPU oracle (oracle/, the only reference this tier has) on a bounded sample.
+Under torchrun (N > 1) the ranks run ONE sharded search (every level's
+work lists are partitioned across ranks, new CSs are all-gathered over NCCL and
+merged canonically; "scaling": "strong"); ``--multi replicas`` runs N independent
+searches instead ("scaling": "weak").  Time is the max over ranks.
+``--impl reference`` times the CPU oracle (oracle/, the only reference this tier
+has) on a bounded sample.
 """
 from __future__ import annotations
 
@@ -39,6 +42,11 @@ WORKLOADS = {
     "table1-row8": (specgen.TABLE1_ROW8, 400,
                     "Table 1 row 8 (P:1352): same spec, costs (10,10,10,1,10), solve to c*"),
     "c1-toy": (specgen.C1_TOY, 40, "BASELINE configs[0] paper-style toy"),
+    "c2-t1-s0": (specgen.gen_type1("01", 6, 10, 10, 0), 40,
+                 "BASELINE configs[1]: Type 1 (P:1239-1242) binary, le=6, p=n=10, SplitMix64 seed 0 "
+                 "(|IC|=58, two-word CS, 64-bit-key hash set)"),
+    "c2-t1-s3": (specgen.gen_type1("01", 6, 10, 10, 3), 40,
+                 "BASELINE configs[1]: Type 1 binary, le=6, p=n=10, seed 3 (|IC|=55)"),
 }
 # Paper numbers for the same workload on its own hardware (context):
 PAPER = {
@@ -47,8 +55,8 @@ PAPER = {
     "table1-row8": {"reps": 23349552935, "gpu_s": 4.9096, "cpu_s": 4519.9456,
                     "hw": "Colab A100-SXM4-40GB (P:1147-1153)"},
 }
-ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8}   # cpu_baseline sample
-REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8}  # --impl reference step
+ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8, "c2-t1-s0": 16, "c2-t1-s3": 16}   # cpu_baseline sample
+REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8, "c2-t1-s0": 14, "c2-t1-s3": 14}  # --impl reference step
 
 METRIC = "candidate REs/sec"
 UNIT = "cand/s"

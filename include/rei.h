@@ -48,6 +48,11 @@ typedef struct {
 #define REI_FLAG_COMPLETE_FINAL_LEVEL 1u /* finish level c* instead of stopping at the
                                             first precise CS (for full level counts)  */
 #define REI_FLAG_NO_EARLY_EXIT REI_FLAG_COMPLETE_FINAL_LEVEL
+#define REI_FLAG_NO_ONTHEFLY 2u          /* stop with REI_OUT_OF_MEMORY as soon as the cache
+                                            is full instead of switching to OnTheFly mode
+                                            (check candidates built from cached
+                                            levels without caching them, until a level needs
+                                            an uncached one)                              */
 
 typedef struct {
   int device;                /* CUDA device ordinal; -1 = the current device             */
@@ -59,6 +64,8 @@ typedef struct {
   int world_size;            /* 0 or 1 = single GPU                                       */
   int rank;
   const void* nccl_unique_id;/* 128-byte ncclUniqueId, broadcast by the caller (rank 0's) */
+  uint64_t max_entries;      /* cap on cached CSs (the language cache size); 0 = set by the
+                                memory budget only                                         */
 } rei_options;
 
 /* Result of rei_solve.  `regex` is owned by the context and valid until the next
@@ -81,7 +88,9 @@ typedef struct {
 /* Per-cost-level statistics (one entry per non-empty level, ascending cost). */
 typedef struct {
   uint32_t cost;
-  uint32_t complete;           /* 1 if the level was fully enumerated                   */
+  uint32_t complete;           /* 1 if the level was fully enumerated and cached; 2 if it
+                                  was fully checked in OnTheFly mode (not cached, unique = 0);
+                                  0 if the search stopped inside it                       */
   uint64_t cand_q, cand_s, cand_c, cand_u; /* candidates by outermost constructor (A9)  */
   uint64_t unique;             /* new unique CSs appended at this level                 */
   uint64_t evaluated;          /* candidates actually evaluated (== sum of cand_* when complete) */

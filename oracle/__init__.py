@@ -52,7 +52,8 @@ def _load():
         lib.orc_masks.argtypes = [c.c_void_p, c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)]
         lib.orc_op.argtypes = [c.c_void_p, c.c_int, c.POINTER(c.c_uint64),
                                c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)]
-        lib.orc_solve.argtypes = [c.c_void_p, c.c_int, c.c_long, c.c_long, c.c_int, c.c_ulonglong]
+        lib.orc_solve.argtypes = [c.c_void_p, c.c_int, c.c_long, c.c_long, c.c_int, c.c_ulonglong, c.c_int]
+        lib.orc_otf_level.argtypes = [c.c_void_p]
         lib.orc_result.argtypes = [c.c_void_p, c.POINTER(c.c_longlong), c.POINTER(c.c_double)]
         lib.orc_regex.argtypes = [c.c_void_p, c.c_char_p, c.c_int]
         lib.orc_num_stats.argtypes = [c.c_void_p]
@@ -181,10 +182,13 @@ class Oracle:
 
     # ---- search --------------------------------------------------------
     def solve(self, max_cost: int = 500, error: Optional[Tuple[int, int]] = None,
-              complete_final_level: bool = False, max_entries: int = 0) -> Result:
+              complete_final_level: bool = False, max_entries: int = 0,
+              onthefly: bool = False) -> Result:
+        """max_entries caps the language cache (0 = unlimited); with onthefly the
+        level that overflows and later ones are only checked."""
         num, den = error if error else (0, 1)
         self._lib.orc_solve(self._h, int(max_cost), int(num), int(den),
-                            1 if complete_final_level else 0, int(max_entries))
+                            1 if complete_final_level else 0, int(max_entries), 1 if onthefly else 0)
         out6 = (ctypes.c_longlong * 6)()
         secs = ctypes.c_double()
         self._lib.orc_result(self._h, out6, ctypes.byref(secs))
@@ -199,6 +203,11 @@ class Oracle:
         return Result(STATUS.get(int(out6[1]), str(out6[1])), buf.value.decode(),
                       int(out6[0]), int(out6[2]), int(out6[3]), int(out6[4]), int(out6[5]),
                       secs.value, levels)
+
+    @property
+    def otf_level(self) -> int:
+        """First cost level checked on the fly (not cached) by the last solve; 0 = none."""
+        return self._lib.orc_otf_level(self._h)
 
     def level_cs(self, cost: int) -> List[int]:
         m = self._lib.orc_level_size(self._h, cost)

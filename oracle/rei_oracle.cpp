@@ -270,6 +270,13 @@ struct Oracle {
   bool oom = false;
   uint64_t n_entries = 0;
 
+  // OnTheFly: once the cache is full, a level is only checked --
+  // candidates are neither deduplicated nor cached (reading B3: the whole level that
+  // overflowed is re-run this way).  checking = true while such a level runs.
+  bool onthefly = false;
+  bool checking = false;
+  int otf_level = 0;  // first level not cached (0 = none)
+
   // One candidate: Alg. 2 lines 15-20.  Every candidate is
   // counted (reading A9) and tested (reading A11).
   void emit(const CS& cs, const Prov& prov) {
@@ -277,11 +284,30 @@ struct Oracle {
     if (!found) ++candidates;
     bool sat = satisfies(cs);
     if (sat && !found) { found = true; found_prov = prov; }
+    if (checking) return;
     if (seen.count(cs)) return;
     if (max_entries && n_entries >= max_entries) { oom = true; return; }
     seen.insert(cs);
     cur->push_back({cs, prov});
     ++n_entries;
+  }
+
+  // Level `cost` needs a level that OnTheFly did not cache?
+  bool needs_uncached(int cost) {
+    if (!otf_level) return false;
+    const int c1 = c[0], c2 = c[1], c3 = c[2], c4 = c[3], c5 = c[4];
+    auto unk = [&](int L) { return L >= otf_level; };
+    auto maybe = [&](int L) { return L >= c1 && (unk(L) || has_level(L)); };
+    if (unk(cost - c2) || unk(cost - c3)) return true;
+    for (int L = c1; L <= cost - c4 - c1; ++L) {
+      int R = cost - c4 - L;
+      if ((unk(L) && maybe(R)) || (unk(R) && maybe(L))) return true;
+    }
+    for (int L = c1; L <= cost - c5 - L; ++L) {
+      int R = cost - c5 - L;
+      if ((unk(L) && maybe(R)) || (unk(R) && maybe(L))) return true;
+    }
+    return false;
   }
 
   bool has_level(int cost) const {
@@ -293,6 +319,7 @@ struct Oracle {
     auto t0 = std::chrono::steady_clock::now();
     levels.clear(); seen.clear(); stats.clear();
     candidates = 0; cand_complete = 0; found = false; oom = false; n_entries = 0;
+    checking = false; otf_level = 0;
     last_complete_cost = 0; regex.clear(); result_cost = 0;
     auto done = [&](int st) {
       status = st;
@@ -332,7 +359,12 @@ struct Oracle {
     last_complete_cost = c1;
 
     // Alg.1 lines 4-9.
+    otf_level = 0;
+    checking = false;
     for (int cost = c1 + 1; cost <= max_cost; ++cost) {
+     if (needs_uncached(cost)) return done(3);  // OnTheFly ran out of cached operands
+     const uint64_t cand_before = candidates, entries_before = n_entries;
+     for (int attempt = 0; attempt < 2; ++attempt) {
       std::vector<Entry> fresh;
       cur = &fresh;
       LevelStat st{cost, 0, 0, 0, 0, 0, 0};
@@ -382,12 +414,23 @@ struct Oracle {
       st.cand_u = cand_level;
       (void)stop_emitting;
 
-      st.unique = fresh.size();
+      if (oom && onthefly && !checking) {
+        // the cache is full: forget this level's entries and check it on the fly
+        for (auto& e : fresh) seen.erase(e.cs);
+        n_entries = entries_before;
+        candidates = cand_before;
+        found = false;
+        oom = false;
+        checking = true;
+        otf_level = cost;
+        continue;
+      }
+      st.unique = checking ? 0 : fresh.size();
       bool complete = !oom && (!found || complete_final_level);
-      st.complete = complete ? 1 : 0;
-      if (st.cand_q + st.cand_s + st.cand_c + st.cand_u > 0 || !fresh.empty())
+      st.complete = complete ? (checking ? 2 : 1) : 0;
+      if (st.cand_q + st.cand_s + st.cand_c + st.cand_u > 0 || !fresh.empty() || checking)
         stats.push_back(st);
-      levels[cost] = std::move(fresh);  // Alg.1 line 9
+      if (!checking) levels[cost] = std::move(fresh);  // Alg.1 line 9
       if (found) {
         regex = print(found_prov);
         result_cost = cost;
@@ -397,6 +440,8 @@ struct Oracle {
       if (oom) return done(3);
       cand_complete = candidates;
       last_complete_cost = cost;
+      break;
+     }
     }
     return done(2);
   }
@@ -474,14 +519,17 @@ void orc_op(void* h, int op, const uint64_t* a, const uint64_t* b, uint64_t* out
 }
 
 int orc_solve(void* h, int max_cost, long err_num, long err_den, int complete_final_level,
-              unsigned long long max_entries) {
+              unsigned long long max_entries, int onthefly) {
   auto* o = static_cast<Oracle*>(h);
   o->err_num = err_num;
   o->err_den = err_den > 0 ? err_den : 1;
   o->complete_final_level = complete_final_level != 0;
   o->max_entries = max_entries;
+  o->onthefly = onthefly != 0;
   return o->solve(max_cost);
 }
+
+int orc_otf_level(void* h) { return static_cast<Oracle*>(h)->otf_level; }
 
 // result: cost, status, candidates (through found), cand_complete, last_complete_cost, seconds
 void orc_result(void* h, long long* out6, double* seconds) {

@@ -247,6 +247,12 @@ __device__ __forceinline__ void on_new(const LevelParams& p, const uint32_t (&cs
 template <int W, int G, class RankF>
 __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
                                               const bool (&skip)[G], RankF rank_of) {
+  if (p.otf) {  // OnTheFly: the cache is full -- check only (a cached operand is never precise)
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (valid[g] && !skip[g] && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, rank_of(g));
+    return;
+  }
   constexpr int MODE = DedupOf<W>::mode;
   if (MODE == DEDUP_BITMAP) {
     uint32_t word[G];

@@ -100,6 +100,8 @@ struct Ctx {
   uint32_t err_num = 0, err_den = 1;
   uint32_t flags = 0;
   uint64_t budget = 0;
+  uint64_t entry_limit = 0;  // rei_options.max_entries (0 = budget only)
+  int otf_level = 0;         // first level checked in OnTheFly mode (0 = none)
 
   DeviceTables tab;
   int W32 = 1;
@@ -266,7 +268,7 @@ void fill_params(Ctx* c, LevelParams& p) {
   const uint64_t total = c->P.size() + c->N.size();
   p.max_errors = c->err_num ? (uint32_t)((uint64_t)c->err_num * total / c->err_den) : 0;
   p.early_exit = (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL) ? 0 : 1;
-  p.cap = c->cap;
+  p.cap = c->entry_limit ? std::min<uint64_t>(c->cap, c->entry_limit) : c->cap;
   p.split = c->tab.split;
   p.nsplit = c->tab.nsplit;
   p.ctl = c->ctl;
@@ -505,7 +507,8 @@ rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
 }
 
 rei_status grow(Ctx* c, uint64_t need_entries) {
-  const uint64_t max_cap = c->budget / bytes_per_entry(c);
+  uint64_t max_cap = c->budget / bytes_per_entry(c);
+  if (c->entry_limit) max_cap = std::min<uint64_t>(max_cap, c->entry_limit);
   if (c->cap >= max_cap) return REI_OUT_OF_MEMORY;
   uint64_t nc = std::max<uint64_t>(c->cap * 4, need_entries);
   if (c->mode == DEDUP_BITMAP) nc = std::min<uint64_t>(nc, (1ull << c->tab.n) + 64);
@@ -539,6 +542,7 @@ struct Comm {
 };
 
 void reset_search(Ctx* c) {
+  c->otf_level = 0;
   c->levels.clear();
   c->stats.clear();
   c->regex.clear();
@@ -656,6 +660,7 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   LevelParams p;
   fill_params(c, p);
   p.out_base = begin;
+  p.otf = c->otf_level ? 1 : 0;
   if ((s = reset_ctl(c)) != REI_OK) return s;
   // operand blocks -> device (one small H2D per level).  Concatenation blocks are
   // split by orientation (left or right operand sliced): one launch each.
@@ -713,6 +718,26 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   }
   CUDA_OK(c, cudaGetLastError());
   return REI_OK;
+}
+
+// Does level `cost` need a level that OnTheFly mode checked but did not cache?  A
+// block with an uncached operand level is needed unless its other operand level is
+// known to be empty.
+bool needs_uncached(const Ctx* c, int cost) {
+  const rei_costs& k = c->costs;
+  const int c1 = (int)k.sym;
+  auto unk = [&](int L) { return c->otf_level && L >= c->otf_level; };
+  auto maybe = [&](int L) { return L >= c1 && (unk(L) || level_size(c, L) > 0); };
+  if (unk(cost - (int)k.opt) || unk(cost - (int)k.star)) return true;
+  for (int L = c1; L <= cost - (int)k.cat - c1; ++L) {
+    const int R = cost - (int)k.cat - L;
+    if ((unk(L) && maybe(R)) || (unk(R) && maybe(L))) return true;
+  }
+  for (int L = c1; L <= cost - (int)k.alt - L; ++L) {
+    const int R = cost - (int)k.alt - L;
+    if ((unk(L) && maybe(R)) || (unk(R) && maybe(L))) return true;
+  }
+  return false;
 }
 
 // Algorithm 1 over all ranks of `g` (world = 1: the single-GPU path, no exchange).
@@ -793,6 +818,12 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
   std::vector<Block> cat, uni;
   std::vector<LevelCtl> all;
   for (int cost = c1 + 1; cost <= (int)max_cost; ++cost) {
+    if (c0->otf_level && needs_uncached(c0, cost)) {
+      // OnTheFly mode needs a level it did not cache: stop
+      for (Ctx* c : g.m) c->result.candidates = c->result.cand_complete;
+      return REI_OUT_OF_MEMORY;
+    }
+    const bool otf = c0->otf_level != 0;
     LevelInfo lv;
     lv.cost = cost;
     uint64_t nq, ns, ncat, nuni;
@@ -808,6 +839,7 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     const uint64_t prev = c0->stats.empty() ? 0 : c0->stats.back().unique;
     const uint64_t expect = std::min<uint64_t>(nq + ns + ncat + nuni, (multi ? 8 : 4) * prev + 1024);
     for (Ctx* c : g.m) {
+      if (otf) break;
       if (c->arena_used + expect > c->cap || c->slabs_used + expect / 32 + 2 > c->slab_cap) {
         if ((s = grow(c, c->arena_used + expect)) != REI_OK && s != REI_OUT_OF_MEMORY) return s;
       }
@@ -836,14 +868,27 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
         need = std::max<uint64_t>(need, lv.begin + l.count + 1);
       }
       if (!overflow) break;
-      // capacity exceeded: grow the cache / dedup set and redo the level
+      // capacity exceeded: grow the cache / dedup set and redo the level; when the
+      // budget is exhausted, switch to OnTheFly mode and re-check the level
+      bool to_otf = false;
       for (Ctx* c : g.m) {
         if ((s = grow(c, need)) != REI_OK) {
+          if (s == REI_OUT_OF_MEMORY && !(c0->flags & REI_FLAG_NO_ONTHEFLY) && !c0->otf_level) {
+            to_otf = true;
+            break;
+          }
           for (Ctx* d : g.m) d->result.candidates = d->result.cand_complete;
           return s;
         }
       }
+      if (to_otf) {
+        for (Ctx* c : g.m) {
+          c->otf_level = cost;
+          if ((s = rebuild_dedup(c, c->arena_used)) != REI_OK) return s;  // drop partial inserts
+        }
+      }
     }
+    const bool otf_now = c0->otf_level != 0;
     uint64_t found_rank = ~0ull, evaluated = 0, eval_c = 0, eval_u = 0;
     for (auto& l : all) {
       found_rank = std::min<uint64_t>(found_rank, l.found_rank);
@@ -853,14 +898,14 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     }
     const bool found = found_rank != ~0ull;
     const bool complete = !found || (c0->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
-    uint64_t size = all[g.rank0].count;
-    if (multi && complete) {
+    uint64_t size = otf_now ? 0 : all[g.rank0].count;
+    if (multi && complete && !otf_now) {
       if ((s = exchange_level(g, lv.begin, all, &size)) != REI_OK) return s;
     }
     lv.size = size;
     st.unique = size;
     st.ms = level_ms;
-    st.complete = complete ? 1 : 0;
+    st.complete = complete ? (otf_now ? 2 : 1) : 0;
     st.evaluated = complete ? (nq + ns + ncat + nuni) : evaluated;
     st.eval_c = complete ? ncat : eval_c;
     st.eval_u = complete ? nuni : eval_u;
@@ -885,6 +930,7 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
       c->result.cand_complete = cand;
       c->result.candidates = cand;
       c->result.last_complete_cost = (uint32_t)cost;
+      if (otf_now) continue;  // nothing cached at this level
       // transposed copy of level c (the sliced-operand layout for later levels)
       if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
         if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
@@ -973,6 +1019,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     c->err_den = opts->err_den ? opts->err_den : 1;
     c->flags = opts->flags;
     c->budget = opts->mem_budget_bytes;
+    c->entry_limit = opts->max_entries;
     if (opts->world_size > 1) {
       if (!opts->nccl_unique_id || opts->rank < 0 || opts->rank >= opts->world_size) {
         g_init_error = "multi-GPU context needs rank in [0, world_size) and an ncclUniqueId";

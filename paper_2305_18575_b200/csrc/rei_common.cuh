@@ -72,6 +72,7 @@ struct LevelParams {
   uint32_t max_errors;        // allowed-error budget (misclassified examples)
   uint32_t exact;             // 1 = precise test, 0 = allowed-error test
   uint32_t early_exit;        // 1 = stop at the first precise candidate
+  uint32_t otf;               // OnTheFly level: test every candidate, no dedup / append
   uint64_t item_begin;        // this rank's share [item_begin, total_items) of the work items
   uint64_t total_items;
   uint64_t out_base;          // arena index of the first entry of level c

@@ -18,6 +18,7 @@ REI_OK, REI_EINVAL, REI_NOT_FOUND, REI_OUT_OF_MEMORY, REI_ECUDA, REI_ENCCL = ran
 STATUS_NAMES = {0: "found", 1: "invalid", 2: "not_found", 3: "out_of_memory", 4: "cuda_error",
                 5: "nccl_error"}
 FLAG_COMPLETE_FINAL_LEVEL = 1
+FLAG_NO_ONTHEFLY = 2
 KERNEL_CLASSES = ("precompute", "unary", "concat", "union", "transpose", "other")
 
 
@@ -37,7 +38,7 @@ class _Options(ctypes.Structure):
                 ("mem_budget_bytes", ctypes.c_uint64), ("err_num", ctypes.c_uint32),
                 ("err_den", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("world_size", ctypes.c_int), ("rank", ctypes.c_int),
-                ("nccl_unique_id", ctypes.c_void_p)]
+                ("nccl_unique_id", ctypes.c_void_p), ("max_entries", ctypes.c_uint64)]
 
 
 class _Result(ctypes.Structure):
@@ -113,7 +114,7 @@ def load_library():
 @dataclasses.dataclass
 class LevelStat:
     cost: int
-    complete: bool
+    complete: int  # 1 cached, 2 checked on the fly (not cached), 0 stopped inside
     cand_q: int
     cand_s: int
     cand_c: int
@@ -158,7 +159,7 @@ class Solver:
                  costs: Sequence[int] = (1, 1, 1, 1, 1), device: int = -1, stream=None,
                  mem_budget_bytes: int = 0, error: Optional[Tuple[int, int]] = None,
                  complete_final_level: bool = False, world_size: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None):
+                 nccl_id: Optional[bytes] = None, max_entries: int = 0, onthefly: bool = True):
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
@@ -178,7 +179,9 @@ class Solver:
             opts.err_num, opts.err_den = int(error[0]), int(error[1])
         else:
             opts.err_num, opts.err_den = 0, 1
-        opts.flags = FLAG_COMPLETE_FINAL_LEVEL if complete_final_level else 0
+        opts.flags = (FLAG_COMPLETE_FINAL_LEVEL if complete_final_level else 0) | \
+            (0 if onthefly else FLAG_NO_ONTHEFLY)
+        opts.max_entries = int(max_entries)
         opts.world_size, opts.rank = int(world_size), int(rank)
         costs_c = _Costs(*[int(c) for c in costs])
         self._keep = (_strs(P), _strs(N))
@@ -224,7 +227,7 @@ class Solver:
         self._lib.rei_level_stats(self._h, None, 0, ctypes.byref(n))
         buf = (_LevelStat * max(1, n.value))()
         self._lib.rei_level_stats(self._h, buf, n.value, ctypes.byref(n))
-        return [LevelStat(b.cost, bool(b.complete), b.cand_q, b.cand_s, b.cand_c, b.cand_u,
+        return [LevelStat(b.cost, int(b.complete), b.cand_q, b.cand_s, b.cand_c, b.cand_u,
                           b.unique, b.evaluated, b.eval_c, b.eval_u, b.ms) for b in buf[:n.value]]
 
     def kernel_stats(self) -> Dict[str, Tuple[int, float]]:

@@ -273,3 +273,23 @@ def test_table1_row1_full_vs_golden():
     g2 = gpu_solver(sp, complete_final_level=True)
     r2 = g2.solve(40)
     assert {l.cost: l.unique for l in r2.levels} == {c: w["unique"] for c, w in want.items()}
+
+
+@pytest.mark.parametrize("cap", [40, 80, 120, 160, 200, 300])
+@pytest.mark.parametrize("otf", [True, False])
+def test_onthefly_parity(cap, otf):
+    # f2: the same cache cap on both sides -> same outcome, same last
+    # checked level, same cached level sets below the first OnTheFly level
+    sp = specgen.C1_TOY.with_costs((1, 3, 3, 1, 3))
+    o = oracle.Oracle.from_spec(sp)
+    ro = o.solve(40, max_entries=cap, onthefly=otf)
+    first_otf = o.otf_level or 10 ** 9
+    g = gpu_solver(sp, max_entries=cap, onthefly=otf)
+    rg = g.solve(40)
+    assert rg.status == ro.status
+    assert rg.last_complete_cost == ro.last_complete_cost
+    if ro.status == "found":
+        assert rg.cost == ro.cost
+        assert precise(rg.regex, sp.P, sp.N)
+    for c in range(1, min(first_otf, ro.last_complete_cost + 1)):
+        assert sorted(g.level_cs(c)) == sorted(o.level_cs(c)), c

@@ -330,3 +330,26 @@ def test_golden_table1_row1_if_present():
             lo = cum
         cum += l["cand_q"] + l["cand_s"] + l["cand_c"] + l["cand_u"]
     assert lo <= 26774099142 <= cum
+
+
+# ------------------------------------------------------ f2: OnTheFly mode
+
+@pytest.mark.parametrize("cap", [40, 80, 120, 160, 200, 300, 10 ** 6])
+def test_onthefly_keeps_minimality(cap):
+    # OnTheFly continues from cached levels "without compromising on
+    # minimality and precision"; when it needs an uncached level it stops (OOM).
+    sp = specgen.C1_TOY.with_costs((1, 3, 3, 1, 3))
+    o = oracle.Oracle.from_spec(sp)
+    full = o.solve(40)
+    r = o.solve(40, max_entries=cap, onthefly=True)
+    if r.status == "found":
+        assert r.cost == full.cost
+        assert precise(r.regex, sp.P, sp.N)
+    else:
+        assert r.status == "out_of_memory"
+    plain = o.solve(40, max_entries=cap, onthefly=False)
+    assert plain.status in ("found", "out_of_memory")
+    # OnTheFly checks at least as many levels as the plain cache-limited search
+    assert r.last_complete_cost >= plain.last_complete_cost
+    if cap >= 10 ** 6:
+        assert r.status == plain.status == "found" and o.otf_level == 0
