@@ -47,6 +47,9 @@ WORKLOADS = {
                  "(|IC|=58, two-word CS, 64-bit-key hash set)"),
     "c2-t1-s3": (specgen.gen_type1("01", 6, 10, 10, 3), 40,
                  "BASELINE configs[1]: Type 1 binary, le=6, p=n=10, seed 3 (|IC|=55)"),
+    "c2-t2-s4": (specgen.gen_type2("01", 6, 10, 10, 4), 40,
+                 "BASELINE configs[1]: Type 2 (P:1244-1253) binary, le=6, p=n=10, seed 4 "
+                 "(|IC|=48, c*=25, ~2.7e10 candidates, 1.5e9 cached CSs)"),
 }
 # Paper numbers for the same workload on its own hardware (context):
 PAPER = {
@@ -55,8 +58,8 @@ PAPER = {
     "table1-row8": {"reps": 23349552935, "gpu_s": 4.9096, "cpu_s": 4519.9456,
                     "hw": "Colab A100-SXM4-40GB (P:1147-1153)"},
 }
-ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8, "c2-t1-s0": 16, "c2-t1-s3": 16}   # cpu_baseline sample
-REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8, "c2-t1-s0": 14, "c2-t1-s3": 14}  # --impl reference step
+ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8, "c2-t1-s0": 16, "c2-t1-s3": 16, "c2-t2-s4": 16}   # cpu_baseline sample
+REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8, "c2-t1-s0": 14, "c2-t1-s3": 14, "c2-t2-s4": 14}  # --impl reference step
 
 METRIC = "candidate REs/sec"
 UNIT = "cand/s"

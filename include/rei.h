@@ -181,6 +181,14 @@ rei_status rei_nccl_unique_id(void* out, size_t cap);
  * context ends with the same result and identical cache; `out` receives rank 0's. */
 rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_result* out);
 
+/* ---- many small specifications ----
+ * Solves n independent contexts (each created by rei_init, any devices) with
+ * `threads` host threads; each context runs on its own stream, so the latency-bound
+ * small searches overlap on the GPU.  out[i] / status[i] receive context i's
+ * result and status (the call returns REI_OK once every context was attempted). */
+rei_status rei_solve_batch(void* const* ctxs, size_t n, uint32_t max_cost, int threads, rei_result* out,
+                           rei_status* status);
+
 /* ---- multi-GPU host logic (pure functions, usable without a GPU) ---- */
 
 /* Contiguous share of a flattened candidate / work-item space of size `total` for

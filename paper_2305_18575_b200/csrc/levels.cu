@@ -40,7 +40,7 @@ constexpr int kWarps = 8;  // warps per CTA of the pair kernels
 template <int W> struct Batch { static constexpr int G = (W <= 2) ? 8 : (W == 4 ? 2 : 1); };
 constexpr unsigned long long kEmpty64 = ~0ull;
 constexpr uint32_t kLocked = 0xffffffffu;
-constexpr int kMaxProbe = 1 << 16;
+constexpr int kMaxProbe = 1 << 12;  // at load <= 1/2 a longer chain means the table is full
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
@@ -159,6 +159,8 @@ __device__ bool insert_indexed(const LevelParams& p, const uint32_t (&cs)[W], un
   const uint32_t fp = (uint32_t)(h >> 32) | 1u;
   unsigned long long s = h & p.dedup.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
+    // the level already overflowed: it will be redone after growth -- stop inserting
+    if (do_append && *(volatile unsigned int*)&p.ctl->overflow) return false;
     unsigned long long v = *(volatile unsigned long long*)&p.dedup.table[s];
     if (v == 0) {
       const unsigned long long lock = ((unsigned long long)fp << 32) | kLocked;
@@ -207,6 +209,8 @@ __device__ __forceinline__ bool insert_hash64(const LevelParams& p, unsigned lon
   if (key == kEmpty64) return atomicExch(p.dedup.special, 1u) == 0u;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     if (v == key) return false;
+    // the level already overflowed: it will be redone after growth -- stop inserting
+    if (*(volatile unsigned int*)&p.ctl->overflow) return false;
     if (v == kEmpty64) {
       const unsigned long long old = atomicCAS(&p.dedup.table[s], kEmpty64, key);
       if (old == kEmpty64) return true;

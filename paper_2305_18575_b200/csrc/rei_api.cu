@@ -13,7 +13,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <thread>
 #include <cstdint>
 #include <cstring>
 #include <map>
@@ -495,6 +497,7 @@ void renumber_items(std::vector<Block>& v) {
 rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
   rei_status s = clear_dedup(c);
   if (s != REI_OK) return s;
+  if ((s = reset_ctl(c)) != REI_OK) return s;  // a stale overflow flag would stop the inserts
   if (!entries) return REI_OK;
   LevelParams p;
   fill_params(c, p);
@@ -1303,6 +1306,26 @@ rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_resu
   }
   if (out) *out = g.m[0]->result;
   return s;
+}
+
+rei_status rei_solve_batch(void* const* ctxs, size_t n, uint32_t max_cost, int threads, rei_result* out,
+                           rei_status* status) {
+  if (!ctxs) return REI_EINVAL;
+  if (threads < 1) threads = 1;
+  std::atomic<size_t> next{0};
+  auto worker = [&]() {
+    for (size_t i = next++; i < n; i = next++) {
+      rei_result r{};
+      const rei_status s = rei_solve(ctxs[i], max_cost, &r);
+      if (out) out[i] = r;
+      if (status) status[i] = s;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads && (size_t)t < n; ++t) pool.emplace_back(worker);
+  worker();
+  for (auto& th : pool) th.join();
+  return REI_OK;
 }
 
 void rei_partition(uint64_t total, int G, int g, uint64_t* begin, uint64_t* end) {

@@ -105,6 +105,9 @@ def load_library():
     lib.rei_partition.argtypes = [c.c_uint64, c.c_int, c.c_int, c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)]
     lib.rei_nccl_unique_id.restype = c.c_int
     lib.rei_nccl_unique_id.argtypes = [c.c_void_p, c.c_size_t]
+    lib.rei_solve_batch.restype = c.c_int
+    lib.rei_solve_batch.argtypes = [c.POINTER(c.c_void_p), c.c_size_t, c.c_uint32, c.c_int,
+                                    c.POINTER(_Result), c.POINTER(c.c_int)]
     lib.rei_solve_group.restype = c.c_int
     lib.rei_solve_group.argtypes = [c.POINTER(c.c_void_p), c.c_int, c.c_uint32, c.POINTER(_Result)]
     _lib = lib
@@ -369,6 +372,25 @@ def solve_group(solvers: Sequence["Solver"], max_cost: int = 500) -> Result:
     return Result(STATUS_NAMES[st], (r.regex or b"").decode("latin-1"), r.cost, r.last_complete_cost,
                   r.candidates, r.cand_complete, r.unique, r.seconds, r.n_ic, r.cs_words,
                   s0.level_stats())
+
+
+def solve_batch(solvers: Sequence["Solver"], max_cost: int = 500, threads: int = 8) -> List[Result]:
+    """Independent searches, `threads` host threads, one stream per context (f4)."""
+    lib = load_library()
+    n = len(solvers)
+    arr = (ctypes.c_void_p * max(1, n))(*[s._h.value for s in solvers])
+    res = (_Result * max(1, n))()
+    sts = (ctypes.c_int * max(1, n))()
+    lib.rei_solve_batch(arr, n, int(max_cost), int(threads), res, sts)
+    out = []
+    for i, s in enumerate(solvers):
+        r, st = res[i], sts[i]
+        if st not in (REI_OK, REI_NOT_FOUND, REI_OUT_OF_MEMORY):
+            raise ReiError(st, s._err())
+        out.append(Result(STATUS_NAMES[st], (r.regex or b"").decode("latin-1"), r.cost,
+                          r.last_complete_cost, r.candidates, r.cand_complete, r.unique, r.seconds,
+                          r.n_ic, r.cs_words, s.level_stats()))
+    return out
 
 
 def solve(spec, max_cost: int = 500, **kw) -> Result:
