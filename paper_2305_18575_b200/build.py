@@ -46,5 +46,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_variant(name: str, defines) -> str:
+    """Build librei_b200_<name>.so with extra -D flags (A/B experiments only)."""
+    out = os.path.join(PKG, f"librei_b200_{name}.so")
+    cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "-v" and f != "-Xptxas"], *[f"-D{d}" for d in defines],
+           "-o", out, *[os.path.join(CSRC, f) for f in SOURCES]]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError(f"nvcc failed building variant {name}")
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

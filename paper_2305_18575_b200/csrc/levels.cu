@@ -238,6 +238,72 @@ template <int W> struct DedupOf {
   static constexpr int mode = (W == 1) ? DEDUP_BITMAP : (W == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
 };
 
+// Per-warp staging of new CSs in shared memory: lanes deposit new entries with a
+// ballot prefix, and the warp reserves arena space with ONE atomicAdd per flush (the
+// level counter is a single address; per-candidate appends serialised on it when
+// 7-10 % of the candidates were new).
+constexpr int kStage = 128;  // entries per warp
+#ifdef REI_UNION_NOSTAGE
+constexpr bool kUnionStaged = false;
+#else
+constexpr bool kUnionStaged = true;
+#endif
+template <int W>
+struct WarpStage {
+  uint32_t* cs;               // [kStage][W] (shared)
+  unsigned long long* rank;   // [kStage] (shared)
+  uint32_t n;                 // entries held (warp-uniform)
+};
+
+// Out of line: the flush is rare and must not bloat the probe loop's instruction stream.
+template <int W>
+__device__ __noinline__ void stage_flush_n(LevelCtl* ctl, uint32_t* arena_out, unsigned long long* bp,
+                                           unsigned long long out_base, unsigned long long cap,
+                                           const uint32_t* scs, const unsigned long long* srank, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long base = 0;
+  if (lane == 0) base = atomicAdd(&ctl->count, (unsigned long long)n);
+  base = __shfl_sync(kFull, base, 0);
+  __syncwarp();
+  for (uint32_t i = lane; i < n; i += 32) {
+    const unsigned long long idx = out_base + base + i;
+    if (idx >= cap) {
+      ctl->overflow = 1;
+      continue;
+    }
+#pragma unroll
+    for (int q = 0; q < W; ++q) arena_out[idx * W + q] = scs[i * W + q];
+    bp[idx] = srank[i];
+  }
+  __syncwarp();
+}
+
+template <int W>
+__device__ __forceinline__ void stage_flush(const LevelParams& p, WarpStage<W>& s) {
+  if (s.n == 0) return;
+  stage_flush_n<W>(p.ctl, p.arena_out, p.bp, p.out_base, p.cap, s.cs, s.rank, s.n);
+  s.n = 0;
+}
+
+// Called by all 32 lanes together (converged).
+template <int W>
+__device__ __forceinline__ void stage_push(const LevelParams& p, WarpStage<W>& s, bool isnew,
+                                           const uint32_t (&cs)[W], unsigned long long rank) {
+  const unsigned mask = __ballot_sync(kFull, isnew);
+  if (!mask) return;
+  const uint32_t cnt = __popc(mask);
+  if (s.n + cnt > (uint32_t)kStage) stage_flush<W>(p, s);
+  if (isnew) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t pos = s.n + __popc(mask & ((1u << lane) - 1u));
+#pragma unroll
+    for (int q = 0; q < W; ++q) s.cs[pos * W + q] = cs[q];
+    s.rank[pos] = rank;
+  }
+  s.n += cnt;
+  __syncwarp();
+}
+
 // Precision is tested on the CSs that are new (Alg. 2 lines 16-17): a CS
 // already cached at a lower level cannot be precise, or the search would have stopped
 // there, and a within-level duplicate is tested by the candidate that inserted it.
@@ -248,9 +314,12 @@ __device__ __forceinline__ void on_new(const LevelParams& p, const uint32_t (&cs
   append<W>(p, cs, r);
 }
 
+// stage != nullptr: called by the whole warp in converged code; new CSs go through the
+// warp's shared-memory stage.  stage == nullptr: per-lane warp-aggregated append.
 template <int W, int G, class RankF>
 __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
-                                              const bool (&skip)[G], RankF rank_of) {
+                                              const bool (&skip)[G], RankF rank_of,
+                                              WarpStage<W>* stage = nullptr) {
   if (p.otf) {  // OnTheFly: the cache is full -- check only (a cached operand is never precise)
 #pragma unroll
     for (int g = 0; g < G; ++g)
@@ -258,35 +327,56 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
     return;
   }
   constexpr int MODE = DedupOf<W>::mode;
-  if (MODE == DEDUP_BITMAP) {
-    uint32_t word[G];
+  if (MODE == DEDUP_BITMAP || MODE == DEDUP_HASH64) {
+    bool isnew[G];
+    if (MODE == DEDUP_BITMAP) {
+      uint32_t word[G];
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const bool need = valid[g] && !skip[g];
-      word[g] = need ? p.dedup.bitmap[cs[g][0] >> 5] : kFull;
-    }
+      for (int g = 0; g < G; ++g) {
+        const bool need = valid[g] && !skip[g];
+        word[g] = need ? p.dedup.bitmap[cs[g][0] >> 5] : kFull;
+      }
 #pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const uint32_t bit = 1u << (cs[g][0] & 31);
-      if (!(word[g] & bit)) {
-        const uint32_t old = atomicOr(&p.dedup.bitmap[cs[g][0] >> 5], bit);
-        if (!(old & bit)) on_new<W>(p, cs[g], rank_of, g);
+      for (int g = 0; g < G; ++g) {
+        const uint32_t bit = 1u << (cs[g][0] & 31);
+        isnew[g] = false;
+        if (!(word[g] & bit)) {
+          const uint32_t old = atomicOr(&p.dedup.bitmap[cs[g][0] >> 5], bit);
+          isnew[g] = !(old & bit);
+          if (!stage && isnew[g]) on_new<W>(p, cs[g], rank_of, g);  // rare: direct append
+        }
+      }
+      if (!stage) return;
+    } else {
+      unsigned long long slot[G], val[G], key[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const bool need = valid[g] && !skip[g];
+        key[g] = key64<W>(cs[g]);
+        slot[g] = hash_cs<W>(cs[g]) & p.dedup.mask;
+        val[g] = need ? p.dedup.table[slot[g]] : key[g];
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        isnew[g] = false;
+        if (val[g] != key[g] || key[g] == kEmpty64) {
+          const bool need = valid[g] && !skip[g];
+          isnew[g] = need && insert_hash64(p, key[g], slot[g], val[g]);
+        }
       }
     }
-  } else if (MODE == DEDUP_HASH64) {
-    unsigned long long slot[G], val[G], key[G];
+    // precision on the new CSs, then append
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const bool need = valid[g] && !skip[g];
-      key[g] = key64<W>(cs[g]);
-      slot[g] = hash_cs<W>(cs[g]) & p.dedup.mask;
-      val[g] = need ? p.dedup.table[slot[g]] : key[g];
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      if (val[g] != key[g] || key[g] == kEmpty64) {
-        const bool need = valid[g] && !skip[g];
-        if (need && insert_hash64(p, key[g], slot[g], val[g])) on_new<W>(p, cs[g], rank_of, g);
+      if (stage) {
+        unsigned long long r = 0;
+        if (isnew[g]) {
+          r = rank_of(g);
+          if (satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, r);
+        }
+        stage_push<W>(p, *stage, isnew[g], cs[g], r);
+      } else if (isnew[g]) {
+        on_new<W>(p, cs[g], rank_of, g);
       }
     }
   } else {
@@ -510,6 +600,16 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
   const uint32_t lane = lane_id();
   const uint32_t lanebit = 1u << lane;
   const TransposeLane tr(lane);
+  // this warp's stage for new CSs (after the split table): [kWarps][kStage][W] + ranks
+  WarpStage<W> stage;
+  {
+    uint32_t* st_cs = s_src + MAXK * NW;
+    auto* st_rank = reinterpret_cast<unsigned long long*>(st_cs + kWarps * kStage * W);
+    const uint32_t warp = threadIdx.x >> 5;
+    stage.cs = st_cs + warp * kStage * W;
+    stage.rank = st_rank + warp * kStage;
+    stage.n = 0;
+  }
   // split masks: bit of the uniform operand that enables split k of word q*32+lane
   uint32_t mlo[W][MAXK], mhi[W][MAXK];
 #pragma unroll
@@ -572,6 +672,11 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
       }
       const unsigned long long sj = s * 32 + lane;
       const bool lane_ok = sj < ns;
+      // this lane's sliced operand itself: x.y == y is a cached CS, no probe needed
+      uint32_t y[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) y[q] = 0;
+      if (lane_ok) load_cs<W>(p.arena + (SLICE_A ? blk.a_base : blk.b_base) * W, sj, y);
 
       // one batch of G groups; FULL batches need no per-group bounds test
       auto batch = [&](uint32_t ub, auto full_tag) {
@@ -600,13 +705,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
 #pragma unroll
           for (int q = 0; q < W; ++q) cs[g][q] = tr(acc[q]);
           valid[g] = FULL ? lane_ok : (lane_ok && ui < nu_item);
+#ifdef REI_NO_YFILTER
           skip[g] = cs_equal<W>(cs[g], x);
+#else
+          skip[g] = cs_equal<W>(cs[g], x) || cs_equal<W>(cs[g], y);
+#endif
         }
         evaluated += lane_ok ? min((uint32_t)G, nu_item - ub) : 0u;
         process_batch<W, G>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u0 + ub + g;
           return cand_off + (SLICE_A ? sj * nb + ui : ui * nb + sj);
-        });
+        }, W == 2 ? &stage : nullptr);
       };
       uint32_t ub = 0;
       for (; ub + G <= nu_item; ub += G) batch(ub, std::true_type{});
@@ -615,6 +724,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
     const uint32_t tot = __reduce_add_sync(kFull, evaluated);
     if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
   }
+  if (W == 2) stage_flush<W>(p, stage);
 }
 
 // ============================================================================
@@ -630,6 +740,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
   constexpr int G = Batch<W>::G;
+  WarpStage<W> stage;  // (W <= 2) new CSs staged per warp after the block table
+  {
+    uint32_t* st_cs = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);
+    auto* st_rank = reinterpret_cast<unsigned long long*>(st_cs + kWarps * kStage * W);
+    const uint32_t warp = threadIdx.x >> 5;
+    stage.cs = st_cs + warp * kStage * W;
+    stage.rank = st_rank + warp * kStage;
+    stage.n = 0;
+  }
 
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
@@ -700,12 +819,13 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
           const unsigned long long i = slice_a ? sj : ui;
           const unsigned long long j = slice_a ? ui : sj;
           return cand_off + (tri ? i * na - i * (i + 1) / 2 + (j - i - 1) : i * nb + j);
-        });
+        }, kUnionStaged && W <= 2 ? &stage : nullptr);
       }
     }
     const uint32_t tot = __reduce_add_sync(kFull, evaluated);
     if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_u, (unsigned long long)tot); }
   }
+  if (kUnionStaged && W <= 2) stage_flush<W>(p, stage);
 }
 
 // ============================================================================
@@ -770,6 +890,113 @@ __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x == 0 && te > tb) atomicAdd(&p.ctl->evaluated, te - tb);
+}
+
+// Bit-sliced unary kernel (W32 <= 2): a warp takes a slab of 32 operands.  ? is
+// x | eps per lane.  * runs on the transposed slab: lane w holds X[w] (bit t =
+// operand t's bit w) and builds S[w] = X[w] | OR_{proper (u,v) of w} X[u] & S[v] one
+// word length at a time (v is shorter than w, so S[v] is final when w's round comes),
+// shuffling X[u] and S[v] from their lanes; a transpose turns the 32 slices into the
+// 32 operands' stars (same fixpoint as star_cs).
+template <int W, int MAXK>
+__global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned long long n_q, unsigned long long n_s,
+                                                    unsigned long long base_q, unsigned long long base_s,
+                                                    unsigned long long slab_s) {
+  static_assert(W <= 2, "sliced unary kernel is for one- and two-word CSs");
+  constexpr int NW = 32 * W;
+  const uint32_t lane = lane_id();
+  const TransposeLane tr(lane);
+  uint32_t len[W], spl[W][MAXK];
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    const uint32_t w = q * 32 + lane;
+    len[q] = w < p.n ? p.word_len[w] : 0u;
+    const uint32_t ns = p.nsplit[w];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) spl[q][k] = (uint32_t)k < ns ? p.split[(size_t)k * kMaxNW + w] : 0xffffffffu;
+  }
+  uint32_t maxlen = 0;
+#pragma unroll
+  for (int q = 0; q < W; ++q) maxlen = max(maxlen, len[q]);
+  maxlen = __reduce_max_sync(kFull, maxlen);
+
+  const unsigned long long total = n_q + n_s;
+  const unsigned long long tb = p.item_begin;  // this rank's operand share [tb, te)
+  const unsigned long long te = total < (unsigned long long)p.total_items ? total : (unsigned long long)p.total_items;
+  const unsigned long long slabs_q = (n_q + 31) / 32, slabs_s = (n_s + 31) / 32;
+  const unsigned long long gwarp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  uint32_t evaluated = 0;
+  constexpr int G = 4;  // slabs per batch: G independent probes per lane in flight
+  const unsigned long long nslab = slabs_q + slabs_s;
+  for (unsigned long long it0 = gwarp * G; it0 < nslab; it0 += nwarps * G) {
+   uint32_t cs[G][W];
+   bool vv[G], skip[G];
+   unsigned long long rk[G];
+#pragma unroll
+   for (int g = 0; g < G; ++g) {
+    const unsigned long long it = it0 + g;
+    const bool star = it >= slabs_q;
+    const unsigned long long s = star ? it - slabs_q : it;
+    const unsigned long long cnt = star ? n_s : n_q;
+    const unsigned long long first = (star ? n_q : 0) + s * 32;  // unary rank of lane 0
+    rk[g] = first + lane;
+    vv[g] = false;
+    skip[g] = true;
+#pragma unroll
+    for (int q = 0; q < W; ++q) cs[g][q] = 0;
+    if (it >= nslab || first >= te || first + 32 <= tb) continue;  // warp-uniform
+    const unsigned long long i = s * 32 + lane;  // operand index within its level
+    const bool valid = i < cnt && first + lane >= tb && first + lane < te;
+    uint32_t x[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) x[q] = 0;
+    if (i < cnt) load_cs<W>(p.arena, (star ? base_s : base_q) + i, x);
+    if (!star) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) cs[g][q] = x[q];
+      cs[g][0] |= 1u;  // x? = eps + x
+    } else {
+      uint32_t X[W], S[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        X[q] = p.tarena[(slab_s + s) * NW + q * 32 + lane];
+        S[q] = (q == 0 && lane == 0) ? kFull : 0u;  // every star contains eps
+      }
+      for (uint32_t L = 1; L <= maxlen; ++L) {
+        uint32_t add[W];
+#pragma unroll
+        for (int q = 0; q < W; ++q) add[q] = 0;
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) {
+            const uint32_t u = spl[q][k] >> 16, v = spl[q][k] & 0xffffu;
+            uint32_t xu = __shfl_sync(kFull, X[0], u & 31), sv = __shfl_sync(kFull, S[0], v & 31);
+            if (W == 2) {
+              const uint32_t xu1 = __shfl_sync(kFull, X[W - 1], u & 31);
+              const uint32_t sv1 = __shfl_sync(kFull, S[W - 1], v & 31);
+              xu = (u & 32) ? xu1 : xu;
+              sv = (v & 32) ? sv1 : sv;
+            }
+            if (spl[q][k] != 0xffffffffu) add[q] |= xu & sv;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+          if (len[q] == L) S[q] = X[q] | add[q];
+      }
+#pragma unroll
+      for (int q = 0; q < W; ++q) cs[g][q] = tr(S[q]);
+    }
+    vv[g] = valid;
+    skip[g] = cs_equal<W>(cs[g], x);
+    evaluated += valid ? 1u : 0u;
+   }
+   process_batch<W, G>(p, cs, vv, skip, [&](int g) { return rk[g]; });
+  }
+  const uint32_t tot = __reduce_add_sync(kFull, evaluated);
+  if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
 }
 
 // Seeds (Alg. 1 line 3): one thread, symbols in Sigma order (deterministic).
@@ -910,7 +1137,8 @@ size_t pair_smem(const LevelParams& p, int W) {
 
 template <int W, int MAXK, bool SA>
 int launch_concat_fast_t(const LevelParams& p, cudaStream_t st) {
-  const size_t smem = p.nblocks * sizeof(Block) + (size_t)MAXK * 32 * W * 4;
+  const size_t smem = p.nblocks * sizeof(Block) + (size_t)MAXK * 32 * W * 4 +
+                      (size_t)kWarps * kStage * (W * 4 + 8);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
@@ -941,16 +1169,34 @@ int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
 
 template <int W>
 int launch_union_t(const LevelParams& p, cudaStream_t st) {
-  const size_t smem = p.nblocks * sizeof(Block);
+  const size_t smem = p.nblocks * sizeof(Block) + (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_union<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_for(k_union<W>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
   k_union<W><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
 
+template <int W, int MAXK>
+int launch_unary_fast_t(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
+                        unsigned long long bq, unsigned long long bs, unsigned long long slab_s, cudaStream_t st) {
+  const unsigned long long slabs = (n_q + 31) / 32 + (n_s + 31) / 32;
+  const int grid = grid_for(k_unary_fast<W, MAXK>, 256, 0, 8, slabs);
+  k_unary_fast<W, MAXK><<<grid, 256, 0, st>>>(p, n_q, n_s, bq, bs, slab_s);
+  return 1;
+}
+
 template <int W>
 int launch_unary_t(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
-                   unsigned long long bq, unsigned long long bs, unsigned long long off_s, cudaStream_t st) {
+                   unsigned long long bq, unsigned long long bs, unsigned long long off_s,
+                   unsigned long long slab_s, cudaStream_t st) {
+  if constexpr (W <= 2) {
+    if (p.maxk <= 15 && !getenv("REI_GENERIC_UNARY")) {
+      if (p.maxk <= 1) return launch_unary_fast_t<W, 1>(p, n_q, n_s, bq, bs, slab_s, st);
+      if (p.maxk <= 3) return launch_unary_fast_t<W, 3>(p, n_q, n_s, bq, bs, slab_s, st);
+      if (p.maxk <= 7) return launch_unary_fast_t<W, 7>(p, n_q, n_s, bq, bs, slab_s, st);
+      return launch_unary_fast_t<W, 15>(p, n_q, n_s, bq, bs, slab_s, st);
+    }
+  }
   const size_t smem = (size_t)p.maxk * 32 * W * 4 + 32 * W * 4;
   if (smem > 48 * 1024) cudaFuncSetAttribute(k_unary<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_for(k_unary<W>, 256, smem, 256, n_q + n_s);
@@ -985,8 +1231,8 @@ int launch_seeds(int W32, const LevelParams& p, const uint32_t* seeds, int nsym,
 }
 
 int launch_unary(int W32, const LevelParams& p, uint64_t n_q, uint64_t n_s, uint64_t bq, uint64_t bs,
-                 uint64_t off_s, cudaStream_t st) {
-  REI_DISPATCH_W(W32, return launch_unary_t<W>(p, n_q, n_s, bq, bs, off_s, st));
+                 uint64_t off_s, uint64_t slab_s, cudaStream_t st) {
+  REI_DISPATCH_W(W32, return launch_unary_t<W>(p, n_q, n_s, bq, bs, off_s, slab_s, st));
 }
 
 int launch_concat(int W32, const LevelParams& p, bool slice_a, cudaStream_t st) {

@@ -273,6 +273,7 @@ void fill_params(Ctx* c, LevelParams& p) {
   p.cap = c->entry_limit ? std::min<uint64_t>(c->cap, c->entry_limit) : c->cap;
   p.split = c->tab.split;
   p.nsplit = c->tab.nsplit;
+  p.word_len = c->tab.word_len;
   p.ctl = c->ctl;
   p.dedup.mode = c->mode;
   p.dedup.bitmap = c->bitmap;
@@ -513,7 +514,8 @@ rei_status grow(Ctx* c, uint64_t need_entries) {
   uint64_t max_cap = c->budget / bytes_per_entry(c);
   if (c->entry_limit) max_cap = std::min<uint64_t>(max_cap, c->entry_limit);
   if (c->cap >= max_cap) return REI_OUT_OF_MEMORY;
-  uint64_t nc = std::max<uint64_t>(c->cap * 4, need_entries);
+  // x8 per growth: every growth rehashes the whole cache, so grow rarely
+  uint64_t nc = std::max<uint64_t>(c->cap * 8, need_entries);
   if (c->mode == DEDUP_BITMAP) nc = std::min<uint64_t>(nc, (1ull << c->tab.n) + 64);
   nc = std::min(nc, max_cap);
   if (nc <= c->cap) return REI_OUT_OF_MEMORY;
@@ -689,11 +691,12 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   if (nq + ns) {
     const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
     const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
+    const uint64_t slab_s = ns ? c->levels.at(cost - (int)k.star).slab : 0;
     LevelParams pq = p;
     if (share(nq + ns, pq)) {
       EventPair ep;
       c->begin_kernel(REI_K_UNARY, ep);
-      int n = launch_unary(c->W32, pq, nq, ns, bq, bs, nq, c->stream);
+      int n = launch_unary(c->W32, pq, nq, ns, bq, bs, nq, slab_s, c->stream);
       c->end_kernel(ep, n);
     }
   }
@@ -1100,7 +1103,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   }
   // bitmap mode: at most 2^n distinct CSs exist, so reserve them all up front (up to
   // 2^28 entries); hash modes start at 2^20 entries and grow ahead of each level.
-  uint64_t cap0 = 1ull << 20;
+  uint64_t cap0 = 1ull << 22;
   if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(1ull << 28, (1ull << c->tab.n) + 64);
   cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, c->budget / bytes_per_entry(c.get())));
   if (alloc_arena(c.get(), cap0, 0, 0) != REI_OK) return fail(c->err);

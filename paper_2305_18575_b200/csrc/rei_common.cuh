@@ -79,6 +79,7 @@ struct LevelParams {
   uint64_t cap;               // arena capacity in entries
   const uint32_t* split;      // [k][kMaxNW] packed (u << 16) | v proper splits
   const uint32_t* nsplit;     // [kMaxNW] number of proper splits per word
+  const uint32_t* word_len;   // [kMaxNW] length of each IC word
   LevelCtl* ctl;
   Dedup dedup;
   uint32_t pos[kMaxW32];

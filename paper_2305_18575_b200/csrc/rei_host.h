@@ -30,7 +30,7 @@ bool run_precompute(const std::vector<std::vector<uint8_t>>& P, const std::vecto
 // Kernel launchers (levels.cu).  Each returns the number of kernels launched.
 int launch_seeds(int W32, const LevelParams& p, const uint32_t* seeds, int nsym, cudaStream_t st);
 int launch_unary(int W32, const LevelParams& p, uint64_t n_q, uint64_t n_s, uint64_t a_base_q,
-                 uint64_t a_base_s, uint64_t off_s, cudaStream_t st);
+                 uint64_t a_base_s, uint64_t off_s, uint64_t slab_s, cudaStream_t st);
 int launch_concat(int W32, const LevelParams& p, bool slice_a, cudaStream_t st);
 int launch_union(int W32, const LevelParams& p, cudaStream_t st);
 int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t count, uint32_t* tarena,

@@ -12,7 +12,8 @@ import os
 from typing import Dict, List, Optional, Sequence, Tuple
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "librei_b200.so")
+# REI_LIB selects an alternative build (A/B experiments, scripts/ab_variants.py)
+LIB_PATH = os.environ.get("REI_LIB") or os.path.join(_PKG, "librei_b200.so")
 
 REI_OK, REI_EINVAL, REI_NOT_FOUND, REI_OUT_OF_MEMORY, REI_ECUDA, REI_ENCCL = range(6)
 STATUS_NAMES = {0: "found", 1: "invalid", 2: "not_found", 3: "out_of_memory", 4: "cuda_error",

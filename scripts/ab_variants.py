@@ -1,0 +1,71 @@
+#!/usr/bin/env python3
+"""A/B timing of compile-time kernel variants on one GPU (experiments only).
+
+    python scripts/ab_variants.py build name:DEF1,DEF2 ...   # here (nvcc, no GPU)
+    python scripts/ab_variants.py run [workload] [reps]      # under gpurun
+
+`run` times every librei_b200*.so found in the package (the default build is
+"base") with REI_LIB, in fresh processes, interleaved, and prints the median
+solve time and per-kernel-class device ms.  Not a bench.py number.
+"""
+import glob
+import json
+import os
+import statistics
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2305_18575_b200")
+sys.path.insert(0, ROOT)
+
+CHILD = r"""
+import json, sys, time
+sys.path.insert(0, %r)
+import bench
+from paper_2305_18575_b200 import Solver
+spec, mc, _ = bench.WORKLOADS[%r]
+s = Solver.from_spec(spec, device=0)
+s.solve(mc)
+out = []
+for _ in range(%d):
+    s.reset_kernel_stats()
+    r = s.solve(mc)
+    out.append({"ms": r.seconds * 1000, "k": s.kernel_stats(), "cand": r.candidates})
+print(json.dumps(out))
+"""
+
+
+def main():
+    if sys.argv[1] == "build":
+        from paper_2305_18575_b200 import build
+        for arg in sys.argv[2:]:
+            name, defs = arg.split(":")
+            print(build.build_variant(name, [d for d in defs.split(",") if d]))
+        return
+    workload = sys.argv[2] if len(sys.argv) > 2 else "table1-row1"
+    reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+    libs = {"base": os.path.join(PKG, "librei_b200.so")}
+    for f in sorted(glob.glob(os.path.join(PKG, "librei_b200_*.so"))):
+        libs[os.path.basename(f)[len("librei_b200_"):-3]] = f
+    res = {k: [] for k in libs}
+    for rnd in range(2):
+        for name, path in libs.items():
+            env = dict(os.environ, REI_LIB=path)
+            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, workload, reps)], env=env,
+                                 capture_output=True, text=True, timeout=600)
+            if out.returncode != 0:
+                print(name, "FAILED", out.stderr[-400:])
+                continue
+            res[name] += json.loads(out.stdout.strip().splitlines()[-1])
+    for name, runs in res.items():
+        if not runs:
+            continue
+        ms = statistics.median(r["ms"] for r in runs)
+        kc = {k: statistics.median(r["k"][k][1] for r in runs) for k in ("concat", "union", "unary")}
+        print(f"{name:16s} solve {ms:8.2f} ms  concat {kc['concat']:7.2f}  union {kc['union']:7.2f}  "
+              f"unary {kc['unary']:6.2f}  ({len(runs)} runs)")
+
+
+if __name__ == "__main__":
+    main()

@@ -153,11 +153,12 @@ def test_search_parity_wide(sp, K):
     compare_search(sp, K)
 
 
+@pytest.mark.parametrize("var", ["REI_GENERIC_CONCAT", "REI_GENERIC_UNARY"])
 @pytest.mark.parametrize("sp,K", RANDOM_W1[:3] + W2[:2], ids=ids(RANDOM_W1[:3] + W2[:2]))
-def test_generic_concat_kernel_parity(sp, K, monkeypatch):
-    # the generic (any split count) concat kernel, used when a word has > 15 proper
-    # splits, exercised on one- and two-word CSs too
-    monkeypatch.setenv("REI_GENERIC_CONCAT", "1")
+def test_generic_kernels_parity(sp, K, var, monkeypatch):
+    # the generic (any split count) concat / unary kernels, used when a word has > 15
+    # proper splits, exercised on one- and two-word CSs too
+    monkeypatch.setenv(var, "1")
     compare_search(sp, K)
 
 
