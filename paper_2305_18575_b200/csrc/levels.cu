@@ -582,10 +582,18 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
 //   * per group the fold is MAXK predicated ORs; the transpose is 3 instructions
 //     per stage (SHFL, funnel rotate, LOP3); G groups are independent chains.
 template <int W, int MAXK, bool SLICE_A>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
+// resident CTAs per SM the register budget is sized for (A/B on B200: one-word CSs run
+// best at 3 CTAs x 8 warps with G = 4 probes per lane; two-word CSs at 2 CTAs)
+#ifndef REI_CONCAT_MINB1
+#define REI_CONCAT_MINB1 3
+#endif
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_concat_fast(LevelParams p) {
   static_assert(W <= 2, "fast path is for one- and two-word CSs");
   constexpr int NW = 32 * W;
-  constexpr int G = (W == 1) ? 8 : 4;  // two-word CSs: fewer groups in flight, no spills
+#ifndef REI_CONCAT_G1
+#define REI_CONCAT_G1 4
+#endif
+  constexpr int G = (W == 1) ? REI_CONCAT_G1 : 4;  // two-word CSs: fewer groups in flight, no spills
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
   uint32_t* s_src = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);  // [MAXK][NW]
@@ -672,11 +680,6 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
       }
       const unsigned long long sj = s * 32 + lane;
       const bool lane_ok = sj < ns;
-      // this lane's sliced operand itself: x.y == y is a cached CS, no probe needed
-      uint32_t y[W];
-#pragma unroll
-      for (int q = 0; q < W; ++q) y[q] = 0;
-      if (lane_ok) load_cs<W>(p.arena + (SLICE_A ? blk.a_base : blk.b_base) * W, sj, y);
 
       // one batch of G groups; FULL batches need no per-group bounds test
       auto batch = [&](uint32_t ub, auto full_tag) {
@@ -705,11 +708,7 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_concat_fast(LevelParams p) {
 #pragma unroll
           for (int q = 0; q < W; ++q) cs[g][q] = tr(acc[q]);
           valid[g] = FULL ? lane_ok : (lane_ok && ui < nu_item);
-#ifdef REI_NO_YFILTER
-          skip[g] = cs_equal<W>(cs[g], x);
-#else
-          skip[g] = cs_equal<W>(cs[g], x) || cs_equal<W>(cs[g], y);
-#endif
+          skip[g] = cs_equal<W>(cs[g], x);  // (an x.y == y filter measured slower: see DESIGN.md)
         }
         evaluated += lane_ok ? min((uint32_t)G, nu_item - ub) : 0u;
         process_batch<W, G>(p, cs, valid, skip, [&](int g) {
@@ -903,6 +902,16 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
                                                     unsigned long long base_q, unsigned long long base_s,
                                                     unsigned long long slab_s) {
   static_assert(W <= 2, "sliced unary kernel is for one- and two-word CSs");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  WarpStage<W> stage;  // new CSs staged per warp: [8 warps][kStage][W] + ranks
+  {
+    uint32_t* st_cs = reinterpret_cast<uint32_t*>(smem_raw);
+    auto* st_rank = reinterpret_cast<unsigned long long*>(st_cs + 8 * kStage * W);
+    const uint32_t warp = threadIdx.x >> 5;
+    stage.cs = st_cs + warp * kStage * W;
+    stage.rank = st_rank + warp * kStage;
+    stage.n = 0;
+  }
   constexpr int NW = 32 * W;
   const uint32_t lane = lane_id();
   const TransposeLane tr(lane);
@@ -993,8 +1002,9 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
     skip[g] = cs_equal<W>(cs[g], x);
     evaluated += valid ? 1u : 0u;
    }
-   process_batch<W, G>(p, cs, vv, skip, [&](int g) { return rk[g]; });
+   process_batch<W, G>(p, cs, vv, skip, [&](int g) { return rk[g]; }, &stage);
   }
+  stage_flush<W>(p, stage);
   const uint32_t tot = __reduce_add_sync(kFull, evaluated);
   if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
 }
@@ -1180,8 +1190,9 @@ template <int W, int MAXK>
 int launch_unary_fast_t(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
                         unsigned long long bq, unsigned long long bs, unsigned long long slab_s, cudaStream_t st) {
   const unsigned long long slabs = (n_q + 31) / 32 + (n_s + 31) / 32;
-  const int grid = grid_for(k_unary_fast<W, MAXK>, 256, 0, 8, slabs);
-  k_unary_fast<W, MAXK><<<grid, 256, 0, st>>>(p, n_q, n_s, bq, bs, slab_s);
+  const size_t smem = (size_t)8 * kStage * (W * 4 + 8);
+  const int grid = grid_for(k_unary_fast<W, MAXK>, 256, smem, 8, slabs);
+  k_unary_fast<W, MAXK><<<grid, 256, smem, st>>>(p, n_q, n_s, bq, bs, slab_s);
   return 1;
 }
 

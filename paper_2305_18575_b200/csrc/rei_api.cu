@@ -48,7 +48,12 @@ NcclApi& nccl_api() {
   static bool tried = false;
   if (tried) return a;
   tried = true;
-  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  void* h = nullptr;
+  if (const char* path = getenv("REI_NCCL_LIB")) {  // the binding points at torch's copy
+    h = dlopen(path, RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+  }
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
   if (!h) return a;
   a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));

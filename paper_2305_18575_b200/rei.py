@@ -172,7 +172,7 @@ class Solver:
         if world_size > 1:
             if nccl_id is None or len(nccl_id) < 128:
                 raise ValueError("world_size > 1 needs the 128-byte nccl_id from rank 0")
-            import torch  # noqa: F401  -- torch's libnccl is the one the library dlopens
+            _use_torch_nccl()
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opts.nccl_unique_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         opts.device = device
@@ -350,9 +350,23 @@ def partition(total: int, G: int, g: int) -> Tuple[int, int]:
     return b.value, e.value
 
 
+def _use_torch_nccl():
+    """Point the library's dlopen at the NCCL build torch loaded (one NCCL per process)."""
+    import torch  # noqa: F401
+    if "REI_NCCL_LIB" in os.environ:
+        return
+    try:
+        import nvidia.nccl
+        cand = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["REI_NCCL_LIB"] = cand
+    except Exception:  # noqa: BLE001 -- fall back to the soname lookup in the library
+        pass
+
+
 def nccl_unique_id() -> bytes:
     """rank 0's ncclUniqueId (128 bytes) for Solver(..., world_size, rank, nccl_id)."""
-    import torch  # noqa: F401  -- load torch's libnccl first; the library dlopens the same one
+    _use_torch_nccl()
     lib = load_library()
     buf = ctypes.create_string_buffer(128)
     st = lib.rei_nccl_unique_id(buf, 128)

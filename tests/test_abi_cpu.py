@@ -63,3 +63,14 @@ def test_sass_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", path],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_nccl_is_resolved_at_run_time(lib):
+    # the library has no link-time NCCL dependency; NCCL is dlopen'ed (torch's copy)
+    # only for multi-GPU contexts -- ncclGetUniqueId works without a GPU
+    import subprocess
+    from paper_2305_18575_b200 import build, nccl_unique_id
+    deps = subprocess.run(["ldd", build.LIB], capture_output=True, text=True).stdout
+    assert "nccl" not in deps
+    a, b = nccl_unique_id(), nccl_unique_id()
+    assert len(a) == 128 and a != b
