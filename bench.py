@@ -214,7 +214,15 @@ def run_ours(args, rank, world, local_rank):
         box = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
         mkw = dict(world_size=world, rank=rank, nccl_id=box[0])
-    solver = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw)
+    multi_note = None
+    try:
+        solver = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw)
+    except Exception as e:  # noqa: BLE001 -- recorded in the JSON line, never silent
+        if not sharded:
+            raise
+        multi_note = f"sharded init failed ({e}); ran independent replicas instead"
+        sharded = False
+        solver = Solver.from_spec(spec, device=local_rank, stream=stream)
     # L2 flush buffer (> 126 MB L2), written between timed steps
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
 
@@ -283,6 +291,7 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- end to end through the public API with host buffers (rei_init + rei_solve + result)
     e2e_s, e2e_cands, h2d, d2h = 0.0, 0, 0, 0
+    init_ms, solve_ms = [], []
     for _ in range(max(1, min(args.steps, 5))):
         with torch.cuda.stream(stream):
             flush.add_(1)
@@ -295,10 +304,14 @@ def run_ours(args, rank, world, local_rank):
             dist.broadcast_object_list(box, src=0)
             mkw2 = dict(world_size=world, rank=rank, nccl_id=box[0])
         s2 = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw2)
+        t_init = time.perf_counter()
         r2 = s2.solve(max_cost)
         _ = r2.regex  # result already copied to the host by rei_solve
         torch.cuda.synchronize()
-        e2e_s += time.perf_counter() - t0
+        t1 = time.perf_counter()
+        e2e_s += t1 - t0
+        init_ms.append(1000 * (t_init - t0))
+        solve_ms.append(1000 * (t1 - t_init))
         e2e_cands += r2.candidates
         hb, db = s2.transfer_bytes()
         h2d += hb
@@ -308,6 +321,7 @@ def run_ours(args, rank, world, local_rank):
     e2e = {"value": e2e_cands / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // n_e2e,
            "d2h_bytes_per_step": d2h // n_e2e,
            "time_to_minimal_re_ms": 1000 * e2e_s / n_e2e,
+           "init_ms_median": statistics.median(init_ms), "solve_ms_median": statistics.median(solve_ms),
            "note": "rei_init (host strings -> device precompute) + rei_solve + result, host wall clock"}
 
     # ---- CPU oracle baseline (rank 0, N=1 only, bounded sample)
@@ -337,6 +351,7 @@ def run_ours(args, rank, world, local_rank):
             "l2": f"{args.flush_mb} MiB buffer written between timed steps (L2 flush)",
             "parallelism": (f"shard{world} (level work lists partitioned, NCCL all-gather of new CSs)"
                             if sharded else f"replicas{world}") if world > 1 else "single",
+            "multi_note": multi_note,
             "paper_context": paper,
             "vs_baseline_note": "value / paper's |REs| per GPU-second on A100 for this spec; the paper's "
                                 "|REs| counting convention differs from reading A9 (DESIGN.md)" if paper else None,

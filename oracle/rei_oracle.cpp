@@ -27,6 +27,15 @@
 //
 // Readings of silent / ambiguous points follow SURVEY.md 8(c) A1-A20 and are
 // listed in DESIGN.md ("Readings").  Candidate counting follows reading A9.
+//
+// Pins (tests/test_oracle_pins.py): E1, the introduction
+// (P:142-161), the Section 5 allowed-error table -- costs and regex text
+// (P:1794-1808), Table 1 row 1's printed regex, brute-force enumeration of
+// syntactic regexes matched with Python re, semiring laws, overfit bound
+// (P:1540-1545), OnTheFly minimality.
+// Parity unpinned: the paper's exact |REs| counts (reading A9 only brackets them
+// between the counts before and after the solution's level) and, in OnTheFly mode,
+// the level at which the cache fills (it depends on the cache size, reading B3).
 
 #include <algorithm>
 #include <array>

@@ -729,7 +729,13 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 // ============================================================================
 // Union kernel: uniform operand x, lane t holds operand_t of the sliced level.
 template <int W>
-__global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
+#ifndef REI_UNION_MINB1
+#define REI_UNION_MINB1 3
+#endif
+#ifndef REI_UNION_G1
+#define REI_UNION_G1 4
+#endif
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : 1) k_union(LevelParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_union(LevelParams p) {
   const uint32_t lane = lane_id();
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
-  constexpr int G = Batch<W>::G;
+  constexpr int G = W == 1 ? REI_UNION_G1 : Batch<W>::G;
   WarpStage<W> stage;  // (W <= 2) new CSs staged per warp after the block table
   {
     uint32_t* st_cs = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);
