@@ -25,6 +25,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
+#include <unordered_map>
 
 #include "rei_common.cuh"
 #include "rei_host.h"
@@ -1135,8 +1136,17 @@ int sm_count() {
 template <typename K>
 int grid_for(K kernel, int threads, size_t smem, unsigned long long work_units_per_cta_hint,
              unsigned long long work) {
+  // the occupancy query costs host microseconds per launch: cache it per (kernel, smem)
+  thread_local std::unordered_map<unsigned long long, int> cache;
+  const unsigned long long key = (unsigned long long)(uintptr_t)(const void*)kernel ^ ((unsigned long long)smem << 48);
   int occ = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    occ = it->second;
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+    cache[key] = occ;
+  }
   if (occ <= 0) occ = 1;
   unsigned long long want = (work + work_units_per_cta_hint - 1) / work_units_per_cta_hint;
   unsigned long long full = (unsigned long long)sm_count() * occ;

@@ -17,6 +17,7 @@
 #include <chrono>
 #include <thread>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -95,6 +96,7 @@ struct LevelInfo {
 struct EventPair {
   cudaEvent_t a, b;
   int cls;
+  cudaStream_t s;
 };
 
 struct Ctx {
@@ -139,6 +141,16 @@ struct Ctx {
   std::string err;
   rei_result result{};
 
+  // concurrent level kernels: 0 = one stream; 1 = ? / * on an auxiliary stream;
+  // 2 = also union on a second one; 3 = as 2 with concat on a high-priority
+  // stream and union on a low-priority one, so union only fills SMs concat
+  // leaves idle (REI_CONCURRENT; the kernels of a level are independent: they
+  // read lower levels and insert through atomics)
+  int concurrency = 0;
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
+
   // multi-rank
   int world = 1, rank = 0;
   void* nccl = nullptr;              // ncclComm_t (one process per GPU)
@@ -168,6 +180,11 @@ struct Ctx {
     cudaFree(d_ctl_all); cudaFree(g_cs); cudaFree(g_bp);
     free_merge_scratch(merge);
     if (nccl) nccl_api().CommDestroy((ncclComm_t)nccl);
+    for (int i = 0; i < 3; ++i) {
+      if (aux[i]) cudaStreamDestroy(aux[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -179,14 +196,15 @@ struct Ctx {
     }
     return ev_pool[ev_next++];
   }
-  void begin_kernel(int cls, EventPair& ep) {
+  void begin_kernel(int cls, EventPair& ep, cudaStream_t s = nullptr) {
     ep.a = next_event();
     ep.b = next_event();
     ep.cls = cls;
-    cudaEventRecord(ep.a, stream);
+    ep.s = s ? s : stream;
+    cudaEventRecord(ep.a, ep.s);
   }
   void end_kernel(EventPair& ep, int n) {
-    cudaEventRecord(ep.b, stream);
+    cudaEventRecord(ep.b, ep.s);
     launches += n;
     k_launches[ep.cls] += n;
     pending.push_back(ep);
@@ -426,7 +444,14 @@ void plan_level(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std::v
   if (cost - (int)k.star < c1) ns = 0;
   if (ns) { lv.plan.push_back({BK_S, cost - (int)k.star, 0, ns, 0, off, ns, false}); off += ns; }
   ncat = 0;
-  const uint64_t target = 8192;  // candidates per work item
+  // candidates per work item: large items amortise the per-slab set-up at deep
+  // levels; small levels get small items so that ~4 items per resident warp
+  // (148 SMs x 24 warps) keep every SM busy instead of a few warps running serially
+  uint64_t pairs = 0;
+  for (int L = c1; L <= cost - (int)k.cat - c1; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.cat - L);
+  for (int L = c1; L <= cost - (int)k.alt - L; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.alt - L);
+  const uint64_t target = std::min<uint64_t>(8192, std::max<uint64_t>(128, pairs / (148 * 24 * 4)));
+  auto tile_u = [&](uint64_t nu) { return std::max<uint64_t>(1, std::min<uint64_t>({64, nu, target / 32})); };
   uint64_t item_off = 0;
   for (int L = c1; L <= cost - (int)k.cat - c1; ++L) {
     const int R = cost - (int)k.cat - L;
@@ -444,7 +469,7 @@ void plan_level(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std::v
     b.cand_off = off; b.cand_count = na * nb;
     const uint64_t nu = b.slice_a ? nb : na, nsl = b.slice_a ? na : nb;
     const uint64_t slabs = (nsl + 31) / 32;
-    b.tu = std::min<uint64_t>(64, nu);
+    b.tu = tile_u(nu);
     b.ts = std::max<uint64_t>(1, std::min<uint64_t>(slabs, target / (32 * b.tu)));
     b.u_tiles = (nu + b.tu - 1) / b.tu;
     b.s_tiles = (slabs + b.ts - 1) / b.ts;
@@ -475,7 +500,7 @@ void plan_level(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std::v
     b.cand_off = off; b.cand_count = cnt;
     const uint64_t nu = b.slice_a ? nb : na, nsl = b.slice_a ? na : nb;
     const uint64_t slabs = (nsl + 31) / 32;
-    b.tu = std::min<uint64_t>(64, nu);
+    b.tu = tile_u(nu);
     b.ts = std::max<uint64_t>(1, std::min<uint64_t>(slabs, target / (32 * b.tu)));
     b.u_tiles = (nu + b.tu - 1) / b.tu;
     b.s_tiles = (slabs + b.ts - 1) / b.ts;
@@ -693,6 +718,16 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     q.total_items = e;
     return e > b;
   };
+  // fork: the level's kernels are independent (they read lower levels and insert
+  // through atomics), so ? / * (and union) may run on auxiliary streams
+  const int conc = c->concurrency;
+  cudaStream_t su = conc >= 1 ? c->aux[0] : c->stream;
+  cudaStream_t sn = conc >= 2 ? c->aux[1] : c->stream;
+  cudaStream_t sc = conc >= 3 ? c->aux[2] : c->stream;
+  if (conc >= 1) {
+    CUDA_OK(c, cudaEventRecord(c->ev_fork, c->stream));
+    for (int i = 0; i < conc; ++i) CUDA_OK(c, cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0));
+  }
   if (nq + ns) {
     const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
     const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
@@ -700,8 +735,8 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     LevelParams pq = p;
     if (share(nq + ns, pq)) {
       EventPair ep;
-      c->begin_kernel(REI_K_UNARY, ep);
-      int n = launch_unary(c->W32, pq, nq, ns, bq, bs, nq, slab_s, c->stream);
+      c->begin_kernel(REI_K_UNARY, ep, su);
+      int n = launch_unary(c->W32, pq, nq, ns, bq, bs, nq, slab_s, su);
       c->end_kernel(ep, n);
     }
   }
@@ -712,8 +747,8 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     pc.nblocks = (uint32_t)catv[r].size();
     if (!share(items_of(catv[r]), pc)) continue;
     EventPair ep;
-    c->begin_kernel(REI_K_CONCAT, ep);
-    int n = launch_concat(c->W32, pc, r == 1, c->stream);
+    c->begin_kernel(REI_K_CONCAT, ep, sc);
+    int n = launch_concat(c->W32, pc, r == 1, sc);
     c->end_kernel(ep, n);
   }
   if (!uni.empty()) {
@@ -722,9 +757,15 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     pu.nblocks = (uint32_t)uni.size();
     if (share(items_of(uni), pu)) {
       EventPair ep;
-      c->begin_kernel(REI_K_UNION, ep);
-      int n = launch_union(c->W32, pu, c->stream);
+      c->begin_kernel(REI_K_UNION, ep, sn);
+      int n = launch_union(c->W32, pu, sn);
       c->end_kernel(ep, n);
+    }
+  }
+  if (conc >= 1) {  // join
+    for (int i = 0; i < conc; ++i) {
+      CUDA_OK(c, cudaEventRecord(c->ev_join[i], c->aux[i]));
+      CUDA_OK(c, cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
     }
   }
   CUDA_OK(c, cudaGetLastError());
@@ -1056,6 +1097,21 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     c->own_stream = true;
   }
   auto fail = [&](const std::string& m) { g_init_error = m; return REI_ECUDA; };
+  {
+    const char* ev = getenv("REI_CONCURRENT");
+    c->concurrency = ev ? std::max(0, std::min(3, atoi(ev))) : 3;
+    if (c->concurrency >= 1) {
+      int prio_lo = 0, prio_hi = 0;
+      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+      for (int i = 0; i < c->concurrency; ++i)
+        if (cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking,
+                                         i == 1 && c->concurrency >= 3 ? prio_lo : prio_hi) != cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+          return fail("auxiliary stream creation failed");
+      if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+        return fail("event creation failed");
+    }
+  }
   if (cudaMalloc(&c->tab.split, sizeof(uint32_t) * kMaxSplitRows * kMaxNW) != cudaSuccess ||
       cudaMalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
       cudaMalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
