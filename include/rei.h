@@ -53,6 +53,22 @@ typedef struct {
                                             (check candidates built from cached
                                             levels without caching them, until a level needs
                                             an uncached one)                              */
+#define REI_FLAG_SHARDED_CACHE 4u        /* multi-GPU capacity mode (not in the
+                                            paper; P:731-734 names memory as the limit): every
+                                            rank holds only the CSs it owns (hash of the CS mod
+                                            world_size) -- dedup slot, cache entry, back-pointer --
+                                            and the level kernels read operands from, and insert
+                                            candidates into, the owners' buffers through peer
+                                            mappings (NVLink P2P / CUDA IPC).  The cache is sized
+                                            once at rei_init (no growth); G ranks hold G x the
+                                            entries of one.  Needs world_size > 1 with `allgather`
+                                            (one process per rank) or rei_solve_group.          */
+
+/* Host all-gather supplied by the caller for REI_FLAG_SHARDED_CACHE across processes
+ * (the binding builds it on torch.distributed): every rank passes `bytes` bytes in
+ * `send`; `recv` receives world_size * bytes, rank order.  Returns 0 on success.  It is
+ * also the per-level barrier of that mode. */
+typedef int (*rei_allgather_fn)(void* user, const void* send, void* recv, size_t bytes);
 
 typedef struct {
   int device;                /* CUDA device ordinal; -1 = the current device             */
@@ -65,7 +81,10 @@ typedef struct {
   int rank;
   const void* nccl_unique_id;/* 128-byte ncclUniqueId, broadcast by the caller (rank 0's) */
   uint64_t max_entries;      /* cap on cached CSs (the language cache size); 0 = set by the
-                                memory budget only                                         */
+                                memory budget only.  With REI_FLAG_SHARDED_CACHE: per rank  */
+  rei_allgather_fn allgather;/* REI_FLAG_SHARDED_CACHE, one process per rank: the host
+                                all-gather (NULL otherwise; nccl_unique_id is then unused) */
+  void* allgather_user;      /* passed back to `allgather`                                */
 } rei_options;
 
 /* Result of rei_solve.  `regex` is owned by the context and valid until the next
@@ -180,6 +199,20 @@ rei_status rei_nccl_unique_id(void* out, size_t cap);
  * 0..G-1 of one sharded search, exchanging through device (peer) copies.  Every
  * context ends with the same result and identical cache; `out` receives rank 0's. */
 rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_result* out);
+
+/* ---- multi-GPU capacity: the sharded cache ----
+ * Contexts created with REI_FLAG_SHARDED_CACHE.  Rank r owns the CSs whose hash
+ * (bits 40.. of the 64-bit CS hash) is r mod G; level c's list is the rank-order
+ * concatenation of the owners' shards.  Every rank enumerates its rei_partition share
+ * of the level's work items (operand blocks = shard pairs, read through peer
+ * mappings), inserts each candidate into its owner's dedup set and appends new CSs
+ * to the owner's shard (remote atomics over NVLink / IPC); there is no list
+ * exchange.  Per level the ranks meet twice (after resetting their control lines and
+ * after their kernels) through the allgather callback, or not at all for virtual
+ * ranks (rei_solve_group), which share one host thread.  Results: the level sizes
+ * and the level CS sets equal the single-GPU search's; the regex and candidate
+ * counts follow the same readings (A9, A11).  rei_level_cs / rei_entry_regex read
+ * across the shards.  Any |IC| <= 512. */
 
 /* ---- many small specifications ----
  * Solves n independent contexts (each created by rei_init, any devices) with

@@ -153,8 +153,9 @@ __device__ __forceinline__ void append(const LevelParams& p, const uint32_t (&cs
 
 // ---- dedup: indexed hash set for wide CSs (fingerprint + arena index).
 // Slot = (fp << 32) | idx, 0 = empty, idx == kLocked while the owner writes the CS.
-template <int W>
-__device__ bool insert_indexed(const LevelParams& p, const uint32_t (&cs)[W], unsigned long long rank,
+// `S` is LevelParams (the local cache) or Peer (the owner's cache, sharded mode).
+template <int W, class S>
+__device__ bool insert_indexed(const S& p, const uint32_t (&cs)[W], unsigned long long rank,
                                bool do_append, unsigned long long known_idx) {
   const unsigned long long h = hash_cs<W>(cs);
   const uint32_t fp = (uint32_t)(h >> 32) | 1u;
@@ -205,7 +206,8 @@ __device__ bool insert_indexed(const LevelParams& p, const uint32_t (&cs)[W], un
 }
 
 // Resolve the insert of a hash64 key whose first slot value is already loaded.
-__device__ __forceinline__ bool insert_hash64(const LevelParams& p, unsigned long long key,
+template <class S>
+__device__ __forceinline__ bool insert_hash64(const S& p, unsigned long long key,
                                               unsigned long long s, unsigned long long v) {
   if (key == kEmpty64) return atomicExch(p.dedup.special, 1u) == 0u;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
@@ -305,6 +307,45 @@ __device__ __forceinline__ void stage_push(const LevelParams& p, WarpStage<W>& s
   __syncwarp();
 }
 
+// Sharded-cache mode (f3): route one candidate to the rank that owns its CS (hash
+// bits 40.. mod shards, independent of the slot bits) and insert it there through
+// the peer mapping; a new entry is appended to the owner's shard of level c.
+// Out of line and with by-value arguments only, so the local-cache kernels keep
+// their hot loops (and their CS arrays in registers) unchanged.
+template <int W>
+struct CsVal {
+  uint32_t w[W];
+};
+
+template <int W>
+__device__ __noinline__ bool sharded_new(const Peer* __restrict__ peers, uint32_t shards, CsVal<W> v,
+                                         unsigned long long rank) {
+  uint32_t cs[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) cs[q] = v.w[q];
+  const unsigned long long h = hash_cs<W>(cs);
+  const Peer& o = peers[(uint32_t)(h >> 40) % shards];
+  constexpr int MODE = DedupOf<W>::mode;
+  if (MODE == DEDUP_HASHIDX) return insert_indexed<W>(o, cs, rank, true, 0);
+  bool isnew;
+  if (MODE == DEDUP_BITMAP) {
+    const uint32_t bit = 1u << (cs[0] & 31);
+    isnew = !(atomicOr(&o.dedup.bitmap[cs[0] >> 5], bit) & bit);
+  } else {
+    const unsigned long long slot = h & o.dedup.mask;
+    isnew = insert_hash64(o, key64<W>(cs), slot, *(volatile unsigned long long*)&o.dedup.table[slot]);
+  }
+  if (!isnew) return false;
+  const unsigned long long idx = o.out_base + atomicAdd(&o.ctl->count, 1ull);
+  if (idx >= o.cap) {
+    o.ctl->overflow = 1;
+    return false;
+  }
+  store_cs<W>(o.arena_out, idx, cs);
+  o.bp[idx] = rank;
+  return true;
+}
+
 // Precision is tested on the CSs that are new (Alg. 2 lines 16-17): a CS
 // already cached at a lower level cannot be precise, or the search would have stopped
 // there, and a within-level duplicate is tested by the candidate that inserted it.
@@ -317,7 +358,7 @@ __device__ __forceinline__ void on_new(const LevelParams& p, const uint32_t (&cs
 
 // stage != nullptr: called by the whole warp in converged code; new CSs go through the
 // warp's shared-memory stage.  stage == nullptr: per-lane warp-aggregated append.
-template <int W, int G, class RankF>
+template <int W, int G, bool SH = false, class RankF>
 __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
                                               const bool (&skip)[G], RankF rank_of,
                                               WarpStage<W>* stage = nullptr) {
@@ -325,6 +366,19 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
 #pragma unroll
     for (int g = 0; g < G; ++g)
       if (valid[g] && !skip[g] && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, rank_of(g));
+    return;
+  }
+  // sharded cache (SH kernels only): every candidate goes to its owner (warp-uniform)
+  if (SH && p.shards > 1) {
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      if (valid[g] && !skip[g]) {
+        CsVal<W> v;
+#pragma unroll
+        for (int q = 0; q < W; ++q) v.w[q] = cs[g][q];
+        const unsigned long long r = rank_of(g);
+        if (sharded_new<W>(p.peers, p.shards, v, r) && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, r);
+      }
     return;
   }
   constexpr int MODE = DedupOf<W>::mode;
@@ -445,7 +499,7 @@ __device__ __forceinline__ bool found_and_stop(const LevelParams& p) {
 // ============================================================================
 // Concatenation kernel.  Dynamic shared memory: split table [maxk][NW], nsplit[NW],
 // blocks[nblocks], and (W > 2) one transposed slab per warp.
-template <int W>
+template <int W, bool SH = false>
 __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
   constexpr int NW = 32 * W;
   constexpr bool kShfl = (W <= 2);
@@ -559,7 +613,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
           evaluated += valid[g] ? 1u : 0u;
         }
         const unsigned long long cand_off = blk.cand_off, nb = blk.nb;
-        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+        process_batch<W, G, SH>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u + g;
           return cand_off + (slice_a ? sj * nb + ui : ui * nb + sj);
         });
@@ -729,7 +783,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 
 // ============================================================================
 // Union kernel: uniform operand x, lane t holds operand_t of the sliced level.
-template <int W>
+template <int W, bool SH = false>
 #ifndef REI_UNION_MINB1
 #define REI_UNION_MINB1 3
 #endif
@@ -820,7 +874,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : 1) k_u
           nvalid += valid[g] ? 1u : 0u;
         }
         evaluated += nvalid;
-        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+        process_batch<W, G, SH>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u0 + ub + g;
           const unsigned long long i = slice_a ? sj : ui;
           const unsigned long long j = slice_a ? ui : sj;
@@ -860,7 +914,7 @@ __device__ void star_cs(const uint32_t (&x)[W], uint32_t (&s)[W], uint32_t n, co
   }
 }
 
-template <int W>
+template <int W, bool SH = false>
 __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long n_q, unsigned long long n_s,
                                                unsigned long long base_q, unsigned long long base_s,
                                                unsigned long long off_s) {
@@ -885,14 +939,14 @@ __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long
 #pragma unroll
       for (int q = 0; q < W; ++q) cs[0][q] = x[q];
       cs[0][0] |= 1u;  // x? = eps + x
-      rank[0] = t;
+      rank[0] = p.rank_base + t;
     } else {
       load_cs<W>(p.arena, base_s + (t - n_q), x);
       star_cs<W>(x, cs[0], p.n, s_split, s_nsplit, NW);
-      rank[0] = off_s + (t - n_q);
+      rank[0] = p.rank_base + off_s + (t - n_q);
     }
     skip[0] = cs_equal<W>(cs[0], x);
-    process_batch<W, 1>(p, cs, valid, skip, [&](int) { return rank[0]; });
+    process_batch<W, 1, SH>(p, cs, valid, skip, [&](int) { return rank[0]; });
   }
   __syncthreads();
   if (threadIdx.x == 0 && blockIdx.x == 0 && te > tb) atomicAdd(&p.ctl->evaluated, te - tb);
@@ -956,7 +1010,7 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
     const unsigned long long s = star ? it - slabs_q : it;
     const unsigned long long cnt = star ? n_s : n_q;
     const unsigned long long first = (star ? n_q : 0) + s * 32;  // unary rank of lane 0
-    rk[g] = first + lane;
+    rk[g] = p.rank_base + first + lane;
     vv[g] = false;
     skip[g] = true;
 #pragma unroll
@@ -1026,7 +1080,7 @@ __global__ void k_seeds(LevelParams p, const uint32_t* seeds, int nsym) {
     for (int q = 0; q < W; ++q) cs[0][q] = seeds[a * kMaxW32 + q];
     bool valid[1] = {true}, skip[1] = {false};
     unsigned long long rank[1] = {(unsigned long long)a};
-    process_batch<W, 1>(p, cs, valid, skip, [&](int) { return rank[0]; });
+    process_batch<W, 1, true>(p, cs, valid, skip, [&](int) { return rank[0]; });
     if (*(volatile unsigned long long*)&p.ctl->found_rank != ~0ull) break;
   }
   p.ctl->evaluated = 0;
@@ -1180,26 +1234,41 @@ int launch_concat_fast_k(const LevelParams& p, cudaStream_t st) {
   return launch_concat_fast_t<W, 15, SA>(p, st);
 }
 
+// Sharded-cache levels (p.shards > 1) run the SH instantiations of the generic
+// kernels: the fast kernels carry no owner routing at all.
+template <int W, bool SH>
+int launch_concat_generic(const LevelParams& p, cudaStream_t st) {
+  const size_t smem = pair_smem(p, W);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_concat<W, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_concat<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
+  k_concat<W, SH><<<grid, kWarps * 32, smem, st>>>(p);
+  return 1;
+}
+
 template <int W>
 int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
+  if (p.shards > 1) return launch_concat_generic<W, true>(p, st);
   if constexpr (W <= 2) {
     if (p.maxk <= 15 && !getenv("REI_GENERIC_CONCAT"))
       return slice_a ? launch_concat_fast_k<W, true>(p, st) : launch_concat_fast_k<W, false>(p, st);
   }
-  const size_t smem = pair_smem(p, W);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_concat<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = grid_for(k_concat<W>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
-  k_concat<W><<<grid, kWarps * 32, smem, st>>>(p);
+  return launch_concat_generic<W, false>(p, st);
+}
+
+template <int W, bool SH>
+int launch_union_sh(const LevelParams& p, cudaStream_t st) {
+  const size_t smem = p.nblocks * sizeof(Block) + (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_union<W, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_union<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
+  k_union<W, SH><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
 
 template <int W>
 int launch_union_t(const LevelParams& p, cudaStream_t st) {
-  const size_t smem = p.nblocks * sizeof(Block) + (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
-  if (smem > 48 * 1024) cudaFuncSetAttribute(k_union<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = grid_for(k_union<W>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
-  k_union<W><<<grid, kWarps * 32, smem, st>>>(p);
-  return 1;
+  return p.shards > 1 ? launch_union_sh<W, true>(p, st) : launch_union_sh<W, false>(p, st);
 }
 
 template <int W, int MAXK>
@@ -1216,6 +1285,14 @@ template <int W>
 int launch_unary_t(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
                    unsigned long long bq, unsigned long long bs, unsigned long long off_s,
                    unsigned long long slab_s, cudaStream_t st) {
+  if (p.shards > 1) {
+    const size_t smem = (size_t)p.maxk * 32 * W * 4 + 32 * W * 4;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_unary<W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = grid_for(k_unary<W, true>, 256, smem, 256, n_q + n_s);
+    k_unary<W, true><<<grid, 256, smem, st>>>(p, n_q, n_s, bq, bs, off_s);
+    return 1;
+  }
   if constexpr (W <= 2) {
     if (p.maxk <= 15 && !getenv("REI_GENERIC_UNARY")) {
       if (p.maxk <= 1) return launch_unary_fast_t<W, 1>(p, n_q, n_s, bq, bs, slab_s, st);

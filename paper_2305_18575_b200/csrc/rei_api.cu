@@ -82,6 +82,7 @@ struct PlanBlock {
   uint64_t na, nb;
   uint64_t cand_off, cand_count;
   bool tri;
+  uint64_t a_off = 0, b_off = 0;  // sharded cache: level index of the operand shards' first entries
 };
 
 struct LevelInfo {
@@ -91,6 +92,9 @@ struct LevelInfo {
   uint64_t slab = 0;    // tarena slab index
   std::vector<PlanBlock> plan;
   bool seeds = false;
+  // sharded cache (f3): owner o's shard = its arena entries [sbegin[o], +ssize[o]),
+  // slabs from sslab[o]; level index soff[o] + i (rank-order concatenation)
+  std::vector<uint64_t> sbegin, ssize, sslab, soff;
 };
 
 struct EventPair {
@@ -127,7 +131,8 @@ struct Ctx {
   unsigned long long* table = nullptr;
   uint64_t slots = 0;
   unsigned int* special = nullptr;
-  LevelCtl* ctl = nullptr;
+  LevelCtl* ctl = nullptr;       // the current level's control line (in ctl_base)
+  LevelCtl* ctl_base = nullptr;  // [2]: sharded mode alternates by level parity
   LevelCtl* h_ctl = nullptr;  // pinned
   Block* d_blocks = nullptr;  // [3][kMaxBlocks]: concat (B sliced), concat (A sliced), union
   Block* h_blocks = nullptr;  // pinned
@@ -146,6 +151,27 @@ struct Ctx {
   // stream and union on a low-priority one, so union only fills SMs concat
   // leaves idle (REI_CONCURRENT; the kernels of a level are independent: they
   // read lower levels and insert through atomics)
+  // sharded cache (f3): every rank's buffers as mapped in this process (self included)
+  bool sharded = false;
+  rei_allgather_fn allgather = nullptr;
+  void* allgather_user = nullptr;
+  struct PeerBuf {
+    uint32_t* arena;
+    unsigned long long* bp;
+    uint32_t* tarena;
+    LevelCtl* ctl_base;
+    uint32_t* bitmap;
+    unsigned long long* table;
+    unsigned int* special;
+    uint64_t cap, slots;
+  };
+  std::vector<PeerBuf> peers;
+  std::vector<void*> ipc_opened;
+  static constexpr int kMaxShards = 64;
+  Peer* d_peers = nullptr;  // [kMaxShards]
+  Peer* h_peers = nullptr;  // pinned
+  std::vector<uint64_t> sh_used, sh_slabs;  // every owner's arena / slab fill
+
   int concurrency = 0;
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
@@ -172,7 +198,9 @@ struct Ctx {
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
     cudaFree(arena); cudaFree(bp); cudaFree(tarena); cudaFree(bitmap); cudaFree(table);
-    cudaFree(special); cudaFree(ctl); cudaFree(d_blocks);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    cudaFree(special); cudaFree(ctl_base); cudaFree(d_blocks); cudaFree(d_peers);
+    if (h_peers) cudaFreeHost(h_peers);
     cudaFree(tab.split); cudaFree(tab.nsplit); cudaFree(tab.word_len); cudaFree(tab.seeds);
     if (h_ctl) cudaFreeHost(h_ctl);
     if (h_blocks) cudaFreeHost(h_blocks);
@@ -355,8 +383,8 @@ Node decode_rank(const Ctx* c, int cost, uint64_t rank) {
     nd.kind = b.kind;
     nd.L = b.L;
     nd.R = b.R;
-    if (b.kind == BK_Q || b.kind == BK_S) { nd.i = t; return nd; }
-    if (!b.tri) { nd.i = t / b.nb; nd.j = t % b.nb; return nd; }
+    if (b.kind == BK_Q || b.kind == BK_S) { nd.i = b.a_off + t; return nd; }
+    if (!b.tri) { nd.i = b.a_off + t / b.nb; nd.j = b.b_off + t % b.nb; return nd; }
     // triangular: start(i) = i*m - i(i+1)/2; largest i with start(i) <= t
     const uint64_t m = b.na;
     uint64_t lo = 0, hi = m - 1;
@@ -365,8 +393,8 @@ Node decode_rank(const Ctx* c, int cost, uint64_t rank) {
       const uint64_t start = mid * m - mid * (mid + 1) / 2;
       if (start <= t) lo = mid; else hi = mid - 1;
     }
-    nd.i = lo;
-    nd.j = t - (lo * m - lo * (lo + 1) / 2) + lo + 1;
+    nd.i = b.a_off + lo;
+    nd.j = b.b_off + t - (lo * m - lo * (lo + 1) / 2) + lo + 1;
     return nd;
   }
   nd.kind = 99;
@@ -382,7 +410,13 @@ bool rebuild(Ctx* c, int cost, uint64_t rank, std::string& out, int& prec, int d
 bool rebuild_entry(Ctx* c, int cost, uint64_t idx, std::string& out, int& prec, int depth) {
   const LevelInfo& lv = c->levels.at(cost);
   unsigned long long r = 0;
-  if (cudaMemcpy(&r, c->bp + lv.begin + idx, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+  const unsigned long long* src = c->bp + lv.begin + idx;
+  if (!lv.ssize.empty()) {  // sharded cache: the entry lives in its owner's shard
+    size_t o = 0;
+    while (o + 1 < lv.ssize.size() && idx >= lv.soff[o] + lv.ssize[o]) ++o;
+    src = c->peers[o].bp + lv.sbegin[o] + (idx - lv.soff[o]);
+  }
+  if (cudaMemcpy(&r, src, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
   c->d2h_bytes += 8;
   return rebuild(c, cost, r, out, prec, depth + 1);
 }
@@ -541,6 +575,7 @@ rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
 }
 
 rei_status grow(Ctx* c, uint64_t need_entries) {
+  if (c->sharded) return REI_OUT_OF_MEMORY;  // peers map the buffers: fixed at rei_init
   uint64_t max_cap = c->budget / bytes_per_entry(c);
   if (c->entry_limit) max_cap = std::min<uint64_t>(max_cap, c->entry_limit);
   if (c->cap >= max_cap) return REI_OUT_OF_MEMORY;
@@ -997,12 +1032,517 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
   return REI_NOT_FOUND;
 }
 
+// ============================================================================
+// Sharded cache: capacity over G ranks.  Rank o owns the CSs whose
+// hash is o mod G; level L's list is the rank-order concatenation of the owners'
+// shards.  Operand blocks are shard pairs read through peer mappings; kernels insert
+// every candidate into its owner's dedup set and shard (levels.cu sharded_new).
+
+// Peer buffer views: virtual ranks (one process) use the group's own pointers.
+void link_local(std::vector<Ctx*>& m) {
+  for (Ctx* c : m) {
+    c->peers.clear();
+    for (Ctx* o : m)
+      c->peers.push_back({o->arena, o->bp, o->tarena, o->ctl_base, o->bitmap, o->table, o->special, o->cap,
+                          o->slots});
+  }
+}
+
+// One process per rank: export every buffer with CUDA IPC, all-gather the handles
+// through the caller's callback, open the other ranks' (collective, at rei_init).
+rei_status link_ipc(Ctx* c) {
+  struct Rec {
+    cudaIpcMemHandle_t h[6];
+    uint64_t cap, slots;
+  };
+  Rec mine{};
+  void* bufs[6] = {c->arena, c->bp, c->tarena, c->ctl_base,
+                   c->mode == DEDUP_BITMAP ? (void*)c->bitmap : (void*)c->table, c->special};
+  for (int i = 0; i < 6; ++i) CUDA_OK(c, cudaIpcGetMemHandle(&mine.h[i], bufs[i]));
+  mine.cap = c->cap;
+  mine.slots = c->slots;
+  std::vector<Rec> all(c->world);
+  if (c->allgather(c->allgather_user, &mine, all.data(), sizeof(Rec)) != 0) {
+    c->err = "allgather callback failed (IPC handle exchange)";
+    return REI_ENCCL;
+  }
+  c->peers.assign(c->world, {});
+  for (int r = 0; r < c->world; ++r) {
+    void* q[6];
+    if (r == c->rank) {
+      for (int i = 0; i < 6; ++i) q[i] = bufs[i];
+    } else {
+      for (int i = 0; i < 6; ++i) {
+        CUDA_OK(c, cudaIpcOpenMemHandle(&q[i], all[r].h[i], cudaIpcMemLazyEnablePeerAccess));
+        c->ipc_opened.push_back(q[i]);
+      }
+    }
+    Ctx::PeerBuf& b = c->peers[r];
+    b.arena = (uint32_t*)q[0];
+    b.bp = (unsigned long long*)q[1];
+    b.tarena = (uint32_t*)q[2];
+    b.ctl_base = (LevelCtl*)q[3];
+    b.bitmap = c->mode == DEDUP_BITMAP ? (uint32_t*)q[4] : nullptr;
+    b.table = c->mode == DEDUP_BITMAP ? nullptr : (unsigned long long*)q[4];
+    b.special = (unsigned int*)q[5];
+    b.cap = all[r].cap;
+    b.slots = all[r].slots;
+  }
+  return REI_OK;
+}
+
+// The kernels address a peer's level through the member's own arena / tarena base
+// (flat 64-bit addresses: offset = byte distance / element size, wrapping), so the
+// operand blocks need no per-block pointer.  Buffers are 2 MB-granular allocations.
+bool peer_offsets_ok(const Ctx* c) {
+  for (const auto& b : c->peers) {
+    const int64_t da = (int64_t)((intptr_t)b.arena - (intptr_t)c->arena);
+    const int64_t dt = (int64_t)((intptr_t)b.tarena - (intptr_t)c->tarena);
+    if (da % (4 * c->W32) || dt % (128 * c->W32)) return false;
+  }
+  return true;
+}
+uint64_t rel_entry(const Ctx* c, int o, uint64_t begin) {
+  return (uint64_t)((int64_t)((intptr_t)c->peers[o].arena - (intptr_t)c->arena) / (4 * c->W32)) + begin;
+}
+uint64_t rel_slab(const Ctx* c, int o, uint64_t slab) {
+  return (uint64_t)((int64_t)((intptr_t)c->peers[o].tarena - (intptr_t)c->tarena) / (128 * c->W32)) + slab;
+}
+
+// Barrier of the ranks of `g` (no-op for virtual ranks: one host thread drives all).
+rei_status group_barrier(Comm& g) {
+  if ((int)g.m.size() == g.world) return REI_OK;
+  Ctx* c = g.m[0];
+  char x = 0;
+  std::vector<char> r(g.world);
+  if (c->allgather(c->allgather_user, &x, r.data(), 1) != 0) {
+    c->err = "allgather callback failed (barrier)";
+    return REI_ENCCL;
+  }
+  return REI_OK;
+}
+
+// Every rank's control line of this level (after the barrier that follows the kernels).
+rei_status read_all_ctl(Comm& g, int parity, std::vector<LevelCtl>& all) {
+  Ctx* c = g.m[0];
+  all.assign(g.world, LevelCtl{});
+  for (int r = 0; r < g.world; ++r)
+    CUDA_OK(c, cudaMemcpy(&all[r], c->peers[r].ctl_base + parity, sizeof(LevelCtl), cudaMemcpyDeviceToHost));
+  c->d2h_bytes += sizeof(LevelCtl) * g.world;
+  return REI_OK;
+}
+
+rei_status upload_peers(Ctx* c, int parity) {
+  const int G = (int)c->peers.size();
+  for (int o = 0; o < G; ++o) {
+    const Ctx::PeerBuf& b = c->peers[o];
+    Peer& q = c->h_peers[o];
+    q.arena_out = b.arena;
+    q.bp = b.bp;
+    q.ctl = b.ctl_base + parity;
+    q.dedup.mode = c->mode;
+    q.dedup.bitmap = b.bitmap;
+    q.dedup.table = b.table;
+    q.dedup.mask = b.slots ? b.slots - 1 : 0;
+    q.dedup.special = b.special;
+    q.out_base = c->sh_used[o];
+    q.cap = c->entry_limit ? std::min<uint64_t>(b.cap, c->entry_limit) : b.cap;
+  }
+  CUDA_OK(c, cudaMemcpyAsync(c->d_peers, c->h_peers, sizeof(Peer) * G, cudaMemcpyHostToDevice, c->stream));
+  c->h2d_bytes += sizeof(Peer) * G;
+  return REI_OK;
+}
+
+struct Shard {
+  int o;
+  uint64_t n, begin, slab, off;
+};
+std::vector<Shard> shards_of(const Ctx* c, int L) {
+  std::vector<Shard> v;
+  auto it = c->levels.find(L);
+  if (it == c->levels.end()) return v;
+  const LevelInfo& lv = it->second;
+  for (size_t o = 0; o < lv.ssize.size(); ++o)
+    if (lv.ssize[o]) v.push_back({(int)o, lv.ssize[o], lv.sbegin[o], lv.sslab[o], lv.soff[o]});
+  return v;
+}
+
+struct UnaryWork {
+  bool star;
+  uint64_t n, base, slab, rank_base;
+};
+
+// The level plan over shard pairs (same candidate multiset as plan_level; the rank
+// space is flattened Q, S, C, U with each operand level taken shard by shard).
+void plan_sharded(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std::vector<Block>& uni,
+                  std::vector<UnaryWork>& un, uint64_t& nq, uint64_t& ns, uint64_t& ncat, uint64_t& nuni) {
+  const rei_costs& k = c->costs;
+  const int c1 = (int)k.sym;
+  uint64_t off = 0;
+  lv.plan.clear();
+  cat.clear();
+  uni.clear();
+  un.clear();
+  nq = ns = ncat = nuni = 0;
+  for (int star = 0; star < 2; ++star) {
+    const int L = cost - (int)(star ? k.star : k.opt);
+    if (L < c1) continue;
+    for (const Shard& a : shards_of(c, L)) {
+      PlanBlock pb{star ? (uint32_t)BK_S : (uint32_t)BK_Q, L, 0, a.n, 0, off, a.n, false};
+      pb.a_off = a.off;
+      lv.plan.push_back(pb);
+      un.push_back({star != 0, a.n, rel_entry(c, a.o, a.begin), rel_slab(c, a.o, a.slab), off});
+      off += a.n;
+      (star ? ns : nq) += a.n;
+    }
+  }
+  uint64_t pairs = 0;
+  for (int L = c1; L <= cost - (int)k.cat - c1; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.cat - L);
+  for (int L = c1; L <= cost - (int)k.alt - L; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.alt - L);
+  const uint64_t target = std::min<uint64_t>(8192, std::max<uint64_t>(128, pairs / (148 * 24 * 4)));
+  auto tile_u = [&](uint64_t nu) { return std::max<uint64_t>(1, std::min<uint64_t>({64, nu, target / 32})); };
+  auto add = [&](std::vector<Block>& v, uint32_t kind, int L, int R, const Shard& a, const Shard& b, bool tri,
+                 uint64_t cnt, uint64_t& item_off) {
+    PlanBlock pb{kind, L, R, a.n, b.n, off, cnt, tri};
+    pb.a_off = a.off;
+    pb.b_off = b.off;
+    lv.plan.push_back(pb);
+    Block x{};
+    x.kind = kind;
+    x.tri = tri ? 1 : 0;
+    x.slice_a = (!tri && a.n > b.n) ? 1 : 0;
+    x.a_base = rel_entry(c, a.o, a.begin);
+    x.b_base = rel_entry(c, b.o, b.begin);
+    x.a_slab = rel_slab(c, a.o, a.slab);
+    x.b_slab = rel_slab(c, b.o, b.slab);
+    x.na = a.n;
+    x.nb = b.n;
+    x.cand_off = off;
+    x.cand_count = cnt;
+    const uint64_t nu = x.slice_a ? b.n : a.n, nsl = x.slice_a ? a.n : b.n;
+    const uint64_t slabs = (nsl + 31) / 32;
+    x.tu = tile_u(nu);
+    x.ts = std::max<uint64_t>(1, std::min<uint64_t>(slabs, target / (32 * x.tu)));
+    x.u_tiles = (nu + x.tu - 1) / x.tu;
+    x.s_tiles = (slabs + x.ts - 1) / x.ts;
+    x.item_off = item_off;
+    item_off += x.u_tiles * x.s_tiles;
+    v.push_back(x);
+    off += cnt;
+  };
+  uint64_t item_off = 0;
+  for (int L = c1; L <= cost - (int)k.cat - c1; ++L) {
+    const int R = cost - (int)k.cat - L;
+    const auto A = shards_of(c, L), B = shards_of(c, R);
+    for (const Shard& a : A)
+      for (const Shard& b : B) {
+        add(cat, BK_C, L, R, a, b, false, a.n * b.n, item_off);
+        ncat += a.n * b.n;
+      }
+  }
+  item_off = 0;
+  for (int L = c1; L <= cost - (int)k.alt - L; ++L) {
+    const int R = cost - (int)k.alt - L;
+    const auto A = shards_of(c, L), B = shards_of(c, R);
+    for (const Shard& a : A)
+      for (const Shard& b : B) {
+        if (L == R && a.o > b.o) continue;  // i < j over the level (A8): shard a before shard b
+        const bool tri = (L == R && a.o == b.o);
+        const uint64_t cnt = tri ? a.n * (a.n - 1) / 2 : a.n * b.n;
+        if (!cnt) continue;
+        add(uni, BK_U, L, R, a, b, tri, cnt, item_off);
+        nuni += cnt;
+      }
+  }
+}
+
+rei_status launch_sharded(Ctx* c, int rank, int world, const std::vector<UnaryWork>& un,
+                          const std::vector<Block>& cat, const std::vector<Block>& uni) {
+  LevelParams p;
+  fill_params(c, p);
+  p.otf = c->otf_level ? 1 : 0;
+  p.shards = (uint32_t)world;
+  p.peers = c->d_peers;
+  std::vector<Block> catv[2];
+  for (const Block& b : cat) catv[b.slice_a ? 1 : 0].push_back(b);
+  for (auto& v : catv) renumber_items(v);
+  const std::vector<Block>* lists[3] = {&catv[0], &catv[1], &uni};
+  for (int r = 0; r < 3; ++r) {
+    if (lists[r]->empty()) continue;
+    std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
+    CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, c->h_blocks + r * Ctx::kMaxBlocks,
+                               lists[r]->size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
+    c->h2d_bytes += lists[r]->size() * sizeof(Block);
+  }
+  auto share = [&](uint64_t total, LevelParams& q) {
+    uint64_t b = 0, e = total;
+    rei_partition(total, world, rank, &b, &e);
+    q.item_begin = b;
+    q.total_items = e;
+    return e > b;
+  };
+  for (const UnaryWork& u : un) {
+    LevelParams pq = p;
+    pq.rank_base = u.rank_base;
+    if (!share(u.n, pq)) continue;
+    EventPair ep;
+    c->begin_kernel(REI_K_UNARY, ep);
+    int n = u.star ? launch_unary(c->W32, pq, 0, u.n, 0, u.base, 0, u.slab, c->stream)
+                   : launch_unary(c->W32, pq, u.n, 0, u.base, 0, 0, 0, c->stream);
+    c->end_kernel(ep, n);
+  }
+  for (int r = 0; r < 2; ++r) {
+    if (catv[r].empty()) continue;
+    LevelParams pc = p;
+    pc.blocks = c->d_blocks + r * Ctx::kMaxBlocks;
+    pc.nblocks = (uint32_t)catv[r].size();
+    if (!share(items_of(catv[r]), pc)) continue;
+    EventPair ep;
+    c->begin_kernel(REI_K_CONCAT, ep);
+    int n = launch_concat(c->W32, pc, r == 1, c->stream);
+    c->end_kernel(ep, n);
+  }
+  if (!uni.empty()) {
+    LevelParams pu = p;
+    pu.blocks = c->d_blocks + 2 * Ctx::kMaxBlocks;
+    pu.nblocks = (uint32_t)uni.size();
+    if (share(items_of(uni), pu)) {
+      EventPair ep;
+      c->begin_kernel(REI_K_UNION, ep);
+      int n = launch_union(c->W32, pu, c->stream);
+      c->end_kernel(ep, n);
+    }
+  }
+  CUDA_OK(c, cudaGetLastError());
+  return REI_OK;
+}
+
+// Start of a level: every member resets its control line of this parity, then the
+// ranks meet (nobody inserts into an owner's line before the owner reset it).
+rei_status begin_sharded_level(Comm& g, int cost) {
+  rei_status s;
+  for (Ctx* c : g.m) {
+    c->ctl = c->ctl_base + (cost & 1);
+    if ((s = reset_ctl(c)) != REI_OK) return s;
+    if ((s = upload_peers(c, cost & 1)) != REI_OK) return s;
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  }
+  return group_barrier(g);
+}
+
+// End of a level: kernels done everywhere, then every rank's control line.
+rei_status end_sharded_level(Comm& g, int cost, std::vector<LevelCtl>& all, double* ms) {
+  rei_status s;
+  for (Ctx* c : g.m) {
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    double t;
+    c->collect_events(&t);
+    if (c == g.m[0] && ms) *ms += t;
+  }
+  if ((s = group_barrier(g)) != REI_OK) return s;
+  return read_all_ctl(g, cost & 1, all);
+}
+
+// Record the shards of a finished level and transpose each member's own shard.
+rei_status commit_shards(Comm& g, LevelInfo& lv, const std::vector<LevelCtl>& all, bool transpose) {
+  const int G = g.world;
+  lv.sbegin.assign(G, 0); lv.ssize.assign(G, 0); lv.sslab.assign(G, 0); lv.soff.assign(G, 0);
+  uint64_t off = 0;
+  for (int o = 0; o < G; ++o) {
+    lv.sbegin[o] = g.m[0]->sh_used[o];
+    lv.sslab[o] = g.m[0]->sh_slabs[o];
+    lv.ssize[o] = all[o].count;
+    lv.soff[o] = off;
+    off += all[o].count;
+  }
+  lv.size = off;
+  for (size_t i = 0; i < g.m.size(); ++i) {
+    Ctx* c = g.m[i];
+    const int me = g.rank0 + (int)i;
+    if (transpose && lv.ssize[me]) {
+      if (lv.sslab[me] + (lv.ssize[me] + 31) / 32 > c->slab_cap) return REI_OUT_OF_MEMORY;
+      EventPair et;
+      c->begin_kernel(REI_K_TRANSPOSE, et);
+      int n = launch_transpose(c->W32, c->arena, lv.sbegin[me], lv.ssize[me], c->tarena, lv.sslab[me], c->stream);
+      c->end_kernel(et, n);
+      CUDA_OK(c, cudaGetLastError());
+    }
+    for (int o = 0; o < G; ++o) {
+      c->sh_used[o] += lv.ssize[o];
+      c->sh_slabs[o] += (lv.ssize[o] + 31) / 32;
+    }
+    c->arena_used = c->sh_used[me];
+    c->slabs_used = c->sh_slabs[me];
+    c->levels[lv.cost] = lv;
+  }
+  return REI_OK;
+}
+
+// Algorithm 1 over a sharded cache (the members of `g` are sharded contexts).
+rei_status solve_sharded(Comm& g, uint32_t max_cost) {
+  Ctx* c0 = g.m[0];
+  const rei_costs& k = c0->costs;
+  const int c1 = (int)k.sym;
+  const int G = g.world;
+  rei_status s;
+  for (Ctx* c : g.m) {
+    reset_search(c);
+    c->sh_used.assign(G, 0);
+    c->sh_slabs.assign(G, 0);
+    if (!peer_offsets_ok(c)) {
+      c->err = "peer buffers are not aligned for flat addressing";
+      return REI_ECUDA;
+    }
+  }
+  uint64_t cand = 1;  // the empty regex (A9)
+  const uint64_t total_ex = c0->P.size() + c0->N.size();
+  const bool empty_ok = c0->P.empty() ||
+                        (c0->err_num && (uint64_t)c0->P.size() * c0->err_den <= (uint64_t)c0->err_num * total_ex);
+  const bool eps_ok = c0->P.size() == 1 && c0->P[0].empty();
+  if (empty_ok || eps_ok) {
+    for (Ctx* c : g.m) {
+      c->regex = empty_ok ? "empty" : "eps";
+      c->result.cost = k.sym;
+      c->result.candidates = cand;
+    }
+    return REI_OK;
+  }
+  // ---- level c1: the symbols (rank 0 inserts them into their owners)
+  for (Ctx* c : g.m) {
+    if ((s = clear_dedup(c)) != REI_OK) return s;
+  }
+  if ((s = begin_sharded_level(g, c1)) != REI_OK) return s;
+  if (g.rank0 == 0) {
+    Ctx* c = g.m[0];
+    LevelParams p;
+    fill_params(c, p);
+    p.shards = (uint32_t)G;
+    p.peers = c->d_peers;
+    EventPair ep;
+    c->begin_kernel(REI_K_OTHER, ep);
+    int n = launch_seeds(c->W32, p, c->tab.seeds, (int)c->alphabet.size(), c->stream);
+    c->end_kernel(ep, n);
+    CUDA_OK(c, cudaGetLastError());
+  }
+  std::vector<LevelCtl> all;
+  double ms0 = 0;
+  if ((s = end_sharded_level(g, c1, all, &ms0)) != REI_OK) return s;
+  {
+    LevelInfo lv;
+    lv.cost = c1;
+    lv.seeds = true;
+    const uint64_t found_seed = all[0].found_rank;
+    if ((s = commit_shards(g, lv, all, found_seed == ~0ull)) != REI_OK) return s;
+    rei_level_stat st{};
+    st.cost = c1;
+    st.unique = lv.size;
+    st.ms = ms0;
+    st.complete = found_seed == ~0ull ? 1 : 0;
+    for (Ctx* c : g.m) c->stats.push_back(st);
+    if (found_seed != ~0ull) {
+      for (Ctx* c : g.m) {
+        c->result.candidates = 1 + found_seed + 1;
+        if ((s = finish_found(c, c1, found_seed)) != REI_OK) return s;
+      }
+      return REI_OK;
+    }
+  }
+  cand += c0->alphabet.size();
+  for (Ctx* c : g.m) {
+    c->result.last_complete_cost = c1;
+    c->result.cand_complete = cand;
+  }
+  std::vector<Block> cat, uni;
+  std::vector<UnaryWork> un;
+  for (int cost = c1 + 1; cost <= (int)max_cost; ++cost) {
+    if (c0->otf_level && needs_uncached(c0, cost)) {
+      for (Ctx* c : g.m) c->result.candidates = c->result.cand_complete;
+      return REI_OUT_OF_MEMORY;
+    }
+    LevelInfo lv;
+    lv.cost = cost;
+    uint64_t nq = 0, ns = 0, ncat = 0, nuni = 0;
+    std::vector<std::vector<Block>> cats(g.m.size()), unis(g.m.size());
+    std::vector<std::vector<UnaryWork>> uns(g.m.size());
+    for (size_t i = 0; i < g.m.size(); ++i)  // same plan on every member; bases are member-relative
+      plan_sharded(g.m[i], cost, lv, cats[i], unis[i], uns[i], nq, ns, ncat, nuni);
+    if (lv.plan.empty()) continue;
+    if ((int)(cats[0].size() + unis[0].size()) > Ctx::kMaxBlocks) {
+      c0->err = "too many operand blocks in one level";
+      return REI_EINVAL;
+    }
+    rei_level_stat st{};
+    st.cost = (uint32_t)cost;
+    st.cand_q = nq; st.cand_s = ns; st.cand_c = ncat; st.cand_u = nuni;
+    double level_ms = 0;
+    for (;;) {
+      if ((s = begin_sharded_level(g, cost)) != REI_OK) return s;
+      for (size_t i = 0; i < g.m.size(); ++i)
+        if ((s = launch_sharded(g.m[i], g.rank0 + (int)i, G, uns[i], cats[i], unis[i])) != REI_OK) return s;
+      if ((s = end_sharded_level(g, cost, all, &level_ms)) != REI_OK) return s;
+      bool overflow = false;
+      for (auto& l : all) overflow |= l.overflow != 0;
+      if (!overflow) break;
+      // an owner's shard is full: OnTheFly -- drop the partial inserts
+      // (each owner rebuilds its dedup set from its cached shards) and re-check the level
+      if ((c0->flags & REI_FLAG_NO_ONTHEFLY) || c0->otf_level) {
+        for (Ctx* c : g.m) c->result.candidates = c->result.cand_complete;
+        return REI_OUT_OF_MEMORY;
+      }
+      for (Ctx* c : g.m) {
+        c->otf_level = cost;
+        if ((s = rebuild_dedup(c, c->arena_used)) != REI_OK) return s;
+        CUDA_OK(c, cudaStreamSynchronize(c->stream));
+      }
+    }
+    const bool otf_now = c0->otf_level != 0;
+    uint64_t found_rank = ~0ull, evaluated = 0, eval_c = 0, eval_u = 0;
+    for (auto& l : all) {
+      found_rank = std::min<uint64_t>(found_rank, l.found_rank);
+      evaluated += l.evaluated;
+      eval_c += l.eval_c;
+      eval_u += l.eval_u;
+    }
+    const bool found = found_rank != ~0ull;
+    const bool complete = !found || (c0->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
+    if (otf_now)
+      for (auto& l : all) l.count = 0;  // nothing cached at an OnTheFly level
+    if ((s = commit_shards(g, lv, all, !found && !otf_now)) != REI_OK) return s;
+    st.unique = lv.size;
+    st.ms = level_ms;
+    st.complete = complete ? (otf_now ? 2 : 1) : 0;
+    st.evaluated = complete ? (nq + ns + ncat + nuni) : evaluated;
+    st.eval_c = complete ? ncat : eval_c;
+    st.eval_u = complete ? nuni : eval_u;
+    for (Ctx* c : g.m) c->stats.push_back(st);
+    if (found) {
+      for (Ctx* c : g.m) {
+        c->result.candidates = cand + st.evaluated;
+        if (complete) {
+          c->result.last_complete_cost = (uint32_t)cost;
+          c->result.cand_complete = cand + st.evaluated;
+        }
+        if ((s = finish_found(c, cost, found_rank)) != REI_OK) return s;
+      }
+      return REI_OK;
+    }
+    cand += nq + ns + ncat + nuni;
+    for (Ctx* c : g.m) {
+      c->result.cand_complete = cand;
+      c->result.candidates = cand;
+      c->result.last_complete_cost = (uint32_t)cost;
+    }
+  }
+  return REI_NOT_FOUND;
+}
+
 rei_status solve_impl(Ctx* c, uint32_t max_cost) {
   Comm g;
   g.m = {c};
   g.world = c->world > 1 ? c->world : 1;
   g.rank0 = c->world > 1 ? c->rank : 0;
   g.nccl = c->nccl;
+  if (c->sharded && c->world > 1) return solve_sharded(g, max_cost);
   return solve_group(g, max_cost);
 }
 
@@ -1072,7 +1612,18 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     c->flags = opts->flags;
     c->budget = opts->mem_budget_bytes;
     c->entry_limit = opts->max_entries;
-    if (opts->world_size > 1) {
+    c->sharded = (opts->flags & REI_FLAG_SHARDED_CACHE) != 0;
+    c->allgather = opts->allgather;
+    c->allgather_user = opts->allgather_user;
+    if (opts->world_size > 1 && c->sharded) {
+      if (!opts->allgather || opts->rank < 0 || opts->rank >= opts->world_size ||
+          opts->world_size > Ctx::kMaxShards) {
+        g_init_error = "sharded-cache context needs rank in [0, world_size <= 64) and an allgather callback";
+        return REI_EINVAL;
+      }
+      c->world = opts->world_size;
+      c->rank = opts->rank;
+    } else if (opts->world_size > 1) {
       if (!opts->nccl_unique_id || opts->rank < 0 || opts->rank >= opts->world_size) {
         g_init_error = "multi-GPU context needs rank in [0, world_size) and an ncclUniqueId";
         return REI_EINVAL;
@@ -1116,14 +1667,17 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       cudaMalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
       cudaMalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
       cudaMalloc(&c->tab.seeds, sizeof(uint32_t) * kMaxW32 * k) != cudaSuccess ||
-      cudaMalloc(&c->ctl, sizeof(LevelCtl)) != cudaSuccess ||
+      cudaMalloc(&c->ctl_base, 2 * sizeof(LevelCtl)) != cudaSuccess ||
+      cudaMalloc(&c->d_peers, sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
+      cudaMallocHost(&c->h_peers, sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
       cudaMalloc(&c->special, sizeof(unsigned int)) != cudaSuccess ||
       cudaMalloc(&c->d_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess ||
       cudaMallocHost(&c->h_ctl, sizeof(LevelCtl)) != cudaSuccess ||
       cudaMallocHost(&c->h_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess)
     return fail(std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError()));
+  c->ctl = c->ctl_base;
   cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
-  if (c->world > 1) {  // one process per GPU: the level exchange runs over NCCL (collective)
+  if (c->world > 1 && !c->sharded) {  // one process per GPU: the level exchange runs over NCCL (collective)
     ncclUniqueId id;
     memcpy(&id, opts->nccl_unique_id, sizeof(id));
     ncclComm_t comm;
@@ -1167,8 +1721,18 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   uint64_t cap0 = 1ull << 22;
   if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(1ull << 28, (1ull << c->tab.n) + 64);
   cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, c->budget / bytes_per_entry(c.get())));
+  if (c->sharded) {  // sized once: peers map these buffers, so they never move
+    cap0 = c->budget / bytes_per_entry(c.get());
+    if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(cap0, (1ull << c->tab.n) + 64);
+    if (c->entry_limit) cap0 = std::min<uint64_t>(cap0, c->entry_limit);
+    cap0 = std::max<uint64_t>(cap0, 1024);
+  }
   if (alloc_arena(c.get(), cap0, 0, 0) != REI_OK) return fail(c->err);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail("init sync failed");
+  if (c->sharded && c->world > 1) {  // collective: map every rank's buffers (CUDA IPC)
+    rei_status st = link_ipc(c.get());
+    if (st != REI_OK) { g_init_error = c->err; return st; }
+  }
   *out = c.release();
   return REI_OK;
 }
@@ -1289,7 +1853,18 @@ rei_status rei_level_cs(const void* ctx, uint32_t cost, uint32_t* out, size_t ca
   if (count) *count = m;
   if (!out || !m) return REI_OK;
   const uint64_t take = std::min<uint64_t>(m, cap);
-  if (cudaMemcpy(out, c->arena + it->second.begin * c->W32, take * 4ull * c->W32, cudaMemcpyDeviceToHost) !=
+  const rei::LevelInfo& lv = it->second;
+  if (!lv.ssize.empty()) {  // sharded cache: the owners' shards in rank order
+    for (size_t o = 0; o < lv.ssize.size(); ++o) {
+      if (lv.soff[o] >= take || !lv.ssize[o]) continue;
+      const uint64_t n = std::min<uint64_t>(lv.ssize[o], take - lv.soff[o]);
+      if (cudaMemcpy(out + lv.soff[o] * c->W32, c->peers[o].arena + lv.sbegin[o] * c->W32, n * 4ull * c->W32,
+                     cudaMemcpyDeviceToHost) != cudaSuccess)
+        return REI_ECUDA;
+    }
+    return REI_OK;
+  }
+  if (cudaMemcpy(out, c->arena + lv.begin * c->W32, take * 4ull * c->W32, cudaMemcpyDeviceToHost) !=
       cudaSuccess)
     return REI_ECUDA;
   return REI_OK;
@@ -1355,7 +1930,12 @@ rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_resu
     g.m.push_back(c);
   }
   const auto t0 = std::chrono::steady_clock::now();
-  rei_status s = rei::solve_group(g, max_cost);
+  int n_sharded = 0;
+  for (Ctx* c : g.m) n_sharded += c->sharded ? 1 : 0;
+  if (n_sharded && n_sharded != G) return REI_EINVAL;
+  if (n_sharded && G > Ctx::kMaxShards) return REI_EINVAL;
+  if (n_sharded) rei::link_local(g.m);
+  rei_status s = n_sharded && G > 1 ? rei::solve_sharded(g, max_cost) : rei::solve_group(g, max_cost);
   const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   std::string first_err;
   for (Ctx* c : g.m)

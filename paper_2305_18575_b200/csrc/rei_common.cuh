@@ -60,6 +60,20 @@ struct Dedup {
   unsigned int* special;            // DEDUP_HASH64: persistent "all-ones key present" flag
 };
 
+// One rank's cache as every rank sees it in sharded-cache mode:
+// the owner of a CS (a hash of its bits) holds its dedup slot, arena entry and
+// back-pointer; other ranks insert through peer mappings of these buffers (NVLink
+// P2P, or CUDA IPC across processes).  Field names match LevelParams, so the insert
+// routines take either.
+struct Peer {
+  uint32_t* arena_out;
+  unsigned long long* bp;
+  LevelCtl* ctl;
+  Dedup dedup;
+  unsigned long long out_base;  // owner's arena index of its shard of level c
+  unsigned long long cap;       // owner's arena capacity
+};
+
 struct LevelParams {
   const uint32_t* arena;      // CS arena (read: operand levels)
   uint32_t* arena_out;        // same buffer (write: level c)
@@ -82,6 +96,10 @@ struct LevelParams {
   const uint32_t* word_len;   // [kMaxNW] length of each IC word
   LevelCtl* ctl;
   Dedup dedup;
+  uint32_t shards;            // sharded-cache mode: number of owners (0/1 = local cache)
+  uint32_t pad_s;
+  const Peer* peers;          // [shards], device memory of this rank
+  uint64_t rank_base;         // unary kernels: rank of their first candidate
   uint32_t pos[kMaxW32];
   uint32_t neg[kMaxW32];
 };

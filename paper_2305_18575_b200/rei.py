@@ -20,6 +20,7 @@ STATUS_NAMES = {0: "found", 1: "invalid", 2: "not_found", 3: "out_of_memory", 4:
                 5: "nccl_error"}
 FLAG_COMPLETE_FINAL_LEVEL = 1
 FLAG_NO_ONTHEFLY = 2
+FLAG_SHARDED_CACHE = 4
 KERNEL_CLASSES = ("precompute", "unary", "concat", "union", "transpose", "other")
 
 
@@ -34,12 +35,51 @@ class _Costs(ctypes.Structure):
                 ("cat", ctypes.c_uint32), ("alt", ctypes.c_uint32)]
 
 
+# rei_allgather_fn: int (*)(void* user, const void* send, void* recv, size_t bytes)
+_ALLGATHER = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                              ctypes.c_size_t)
+
+
 class _Options(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p),
                 ("mem_budget_bytes", ctypes.c_uint64), ("err_num", ctypes.c_uint32),
                 ("err_den", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("world_size", ctypes.c_int), ("rank", ctypes.c_int),
-                ("nccl_unique_id", ctypes.c_void_p), ("max_entries", ctypes.c_uint64)]
+                ("nccl_unique_id", ctypes.c_void_p), ("max_entries", ctypes.c_uint64),
+                ("allgather", _ALLGATHER), ("allgather_user", ctypes.c_void_p)]
+
+
+def torch_allgather(group=None):
+    """Host all-gather over torch.distributed for REI_FLAG_SHARDED_CACHE: bytes -> the
+    ranks' bytes in rank order.  Runs on a gloo group (CPU tensors); with another
+    default backend a gloo group is created (collective: every rank calls this)."""
+    import torch
+    import torch.distributed as dist
+    if group is None and dist.get_backend() != "gloo":
+        group = dist.new_group(backend="gloo")
+    world = dist.get_world_size(group)
+
+    def gather(data: bytes):
+        t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+        out = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(out, t, group=group)
+        return [bytes(o.numpy().tobytes()) for o in out]
+    return gather
+
+
+def c_allgather(fn):
+    """Wrap a Python all-gather (bytes -> list of bytes, rank order) as the C callback."""
+    def cb(user, send, recv, n):
+        try:
+            parts = fn(ctypes.string_at(send, n))
+            buf = b"".join(parts)
+            if any(len(x) != n for x in parts):
+                return 1
+            ctypes.memmove(recv, buf, len(buf))
+            return 0
+        except Exception:  # noqa: BLE001 -- reported to the library as a failed collective
+            return 1
+    return _ALLGATHER(cb)
 
 
 class _Result(ctypes.Structure):
@@ -163,13 +203,21 @@ class Solver:
                  costs: Sequence[int] = (1, 1, 1, 1, 1), device: int = -1, stream=None,
                  mem_budget_bytes: int = 0, error: Optional[Tuple[int, int]] = None,
                  complete_final_level: bool = False, world_size: int = 1, rank: int = 0,
-                 nccl_id: Optional[bytes] = None, max_entries: int = 0, onthefly: bool = True):
+                 nccl_id: Optional[bytes] = None, max_entries: int = 0, onthefly: bool = True,
+                 sharded_cache: bool = False, allgather=None):
+        """sharded_cache: capacity mode (include/rei.h REI_FLAG_SHARDED_CACHE).  With
+        world_size > 1 (one process per rank) `allgather` is a Python all-gather
+        (bytes -> list of bytes); default: torch_allgather() over torch.distributed."""
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
         opts = _Options()
         self._nccl_id = None
-        if world_size > 1:
+        self._allgather = None
+        if world_size > 1 and sharded_cache:
+            self._allgather = c_allgather(allgather or torch_allgather())
+            opts.allgather = self._allgather
+        elif world_size > 1:
             if nccl_id is None or len(nccl_id) < 128:
                 raise ValueError("world_size > 1 needs the 128-byte nccl_id from rank 0")
             _use_torch_nccl()
@@ -184,7 +232,7 @@ class Solver:
         else:
             opts.err_num, opts.err_den = 0, 1
         opts.flags = (FLAG_COMPLETE_FINAL_LEVEL if complete_final_level else 0) | \
-            (0 if onthefly else FLAG_NO_ONTHEFLY)
+            (0 if onthefly else FLAG_NO_ONTHEFLY) | (FLAG_SHARDED_CACHE if sharded_cache else 0)
         opts.max_entries = int(max_entries)
         opts.world_size, opts.rank = int(world_size), int(rank)
         costs_c = _Costs(*[int(c) for c in costs])

@@ -5,7 +5,11 @@
 * the level exchange protocol: ranks all-gather their new-CS lists in rank order
   and keep first occurrences -- every rank derives the same canonical list, equal
   to the union of the lists;
-* bench.py's cross-rank reduction: time = max over ranks, work = sum.
+* bench.py's cross-rank reduction: time = max over ranks, work = sum;
+* the sharded cache's host transport (REI_FLAG_SHARDED_CACHE): the C all-gather
+  callback the binding builds on torch.distributed returns every rank's bytes in
+  rank order (IPC-handle exchange and the per-level barrier go through it), and
+  hash ownership splits a level into disjoint shards that cover it.
 """
 import os
 import random
@@ -59,6 +63,21 @@ def _worker(rank, world, port, q):
         import bench
         t, c = bench.reduce_over_ranks(10.0 + rank, 1000 * (rank + 1), torch.device("cpu"), world)
         assert t == 10.0 + world - 1 and c == sum(1000 * (r + 1) for r in range(world))
+        # 4) sharded-cache transport: the C callback over torch.distributed (gloo)
+        import ctypes
+        from paper_2305_18575_b200.rei import c_allgather, torch_allgather
+        cb = c_allgather(torch_allgather())
+        for n in (1, 7, 400):  # 1 byte = the per-level barrier; 400 = IPC handle records
+            send = ctypes.create_string_buffer(bytes([(rank * 31 + i) % 256 for i in range(n)]), n)
+            recv = ctypes.create_string_buffer(n * world)
+            assert cb(None, ctypes.cast(send, ctypes.c_void_p), ctypes.cast(recv, ctypes.c_void_p), n) == 0
+            want = b"".join(bytes([(r * 31 + i) % 256 for i in range(n)]) for r in range(world))
+            assert recv.raw == want
+        keys = list(range(0, 5000, 7))
+        mine = [k for k in keys if ((k * 0x9E3779B97F4A7C15 & (2 ** 64 - 1)) >> 40) % world == rank]
+        shards = [None] * world
+        dist.all_gather_object(shards, mine)
+        assert sorted(x for sh in shards for x in sh) == keys
         q.put((rank, "ok"))
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e)))
