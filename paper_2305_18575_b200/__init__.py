@@ -4,7 +4,7 @@ The search runs in ``librei_b200.so`` (CUDA, sm_100a); ``rei`` is its ctypes
 binding.  ``build`` compiles the library in-tree.  There is no CPU fallback.
 """
 from .rei import (LevelStat, ReiError, Result, Solver, load_library, nccl_unique_id,  # noqa: F401
-                  partition, solve, solve_batch, solve_group)
+                  partition, release_cached_memory, solve, solve_batch, solve_group)
 
 __all__ = ["Solver", "Result", "LevelStat", "ReiError", "solve", "solve_batch", "solve_group",
-           "nccl_unique_id", "partition", "load_library"]
+           "nccl_unique_id", "partition", "load_library", "release_cached_memory"]

@@ -12,7 +12,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "librei_b200.so")
-SOURCES = ["precompute.cu", "levels.cu", "exchange.cu", "rei_api.cu"]
+SOURCES = ["precompute.cu", "levels.cu", "exchange.cu", "devmem.cu", "rei_api.cu"]
 HEADERS = ["rei_common.cuh", "rei_host.h"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

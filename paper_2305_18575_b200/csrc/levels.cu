@@ -226,6 +226,18 @@ __device__ __forceinline__ bool insert_hash64(const S& p, unsigned long long key
   return false;
 }
 
+// Bitmap position of a one-word CS (dedup over all 2^n languages, |IC| <= 32).
+// REI_BITMAP_REV (A/B experiment): bit-reversed, so the long IC words select the
+// word within a 128-byte line and the short ones the line.
+__device__ __forceinline__ uint32_t bm_pos(uint32_t cs, uint32_t n) {
+#ifdef REI_BITMAP_REV
+  return n ? __brev(cs) >> (32 - n) : 0u;
+#else
+  (void)n;
+  return cs;
+#endif
+}
+
 template <int W>
 __device__ __forceinline__ unsigned long long key64(const uint32_t (&cs)[W]) {
   return W == 1 ? (unsigned long long)cs[0]
@@ -318,8 +330,8 @@ struct CsVal {
 };
 
 template <int W>
-__device__ __noinline__ bool sharded_new(const Peer* __restrict__ peers, uint32_t shards, CsVal<W> v,
-                                         unsigned long long rank) {
+__device__ __noinline__ bool sharded_new(const Peer* __restrict__ peers, uint32_t shards, uint32_t n,
+                                         CsVal<W> v, unsigned long long rank) {
   uint32_t cs[W];
 #pragma unroll
   for (int q = 0; q < W; ++q) cs[q] = v.w[q];
@@ -329,8 +341,9 @@ __device__ __noinline__ bool sharded_new(const Peer* __restrict__ peers, uint32_
   if (MODE == DEDUP_HASHIDX) return insert_indexed<W>(o, cs, rank, true, 0);
   bool isnew;
   if (MODE == DEDUP_BITMAP) {
-    const uint32_t bit = 1u << (cs[0] & 31);
-    isnew = !(atomicOr(&o.dedup.bitmap[cs[0] >> 5], bit) & bit);
+    const uint32_t pos = bm_pos(cs[0], n);
+    const uint32_t bit = 1u << (pos & 31);
+    isnew = !(atomicOr(&o.dedup.bitmap[pos >> 5], bit) & bit);
   } else {
     const unsigned long long slot = h & o.dedup.mask;
     isnew = insert_hash64(o, key64<W>(cs), slot, *(volatile unsigned long long*)&o.dedup.table[slot]);
@@ -377,7 +390,7 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
 #pragma unroll
         for (int q = 0; q < W; ++q) v.w[q] = cs[g][q];
         const unsigned long long r = rank_of(g);
-        if (sharded_new<W>(p.peers, p.shards, v, r) && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, r);
+        if (sharded_new<W>(p.peers, p.shards, p.n, v, r) && satisfies<W>(cs[g], p)) atomicMin(&p.ctl->found_rank, r);
       }
     return;
   }
@@ -385,18 +398,19 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
   if (MODE == DEDUP_BITMAP || MODE == DEDUP_HASH64) {
     bool isnew[G];
     if (MODE == DEDUP_BITMAP) {
-      uint32_t word[G];
+      uint32_t word[G], pos[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const bool need = valid[g] && !skip[g];
-        word[g] = need ? p.dedup.bitmap[cs[g][0] >> 5] : kFull;
+        pos[g] = bm_pos(cs[g][0], p.n);
+        word[g] = need ? p.dedup.bitmap[pos[g] >> 5] : kFull;
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const uint32_t bit = 1u << (cs[g][0] & 31);
+        const uint32_t bit = 1u << (pos[g] & 31);
         isnew[g] = false;
         if (!(word[g] & bit)) {
-          const uint32_t old = atomicOr(&p.dedup.bitmap[cs[g][0] >> 5], bit);
+          const uint32_t old = atomicOr(&p.dedup.bitmap[pos[g] >> 5], bit);
           isnew[g] = !(old & bit);
           if (!stage && isnew[g]) on_new<W>(p, cs[g], rank_of, g);  // rare: direct append
         }
@@ -648,7 +662,12 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 #ifndef REI_CONCAT_G1
 #define REI_CONCAT_G1 4
 #endif
-  constexpr int G = (W == 1) ? REI_CONCAT_G1 : 4;  // two-word CSs: fewer groups in flight, no spills
+  constexpr int G = (W == 1) ? REI_CONCAT_G1 : 4;  // groups (probes per lane) in flight
+  // slabs per pass: keep SB * W * MAXK shuffled slab words in registers (<= 16 + W * MAXK)
+  constexpr int SB0 = (W * MAXK <= 3) ? 4 : (W * MAXK <= 7 ? 2 : 1);
+  constexpr int SB = SB0 < G ? SB0 : G;
+  constexpr int GX = G / SB;  // uniform operands per batch
+  static_assert(G % SB == 0 && 32 % GX == 0, "batch shape");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
   uint32_t* s_src = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);  // [MAXK][NW]
@@ -713,67 +732,84 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
     if (lane < nu_item) load_cs<W>(ubase, u0 + lane, xa);
     if (lane + 32 < nu_item) load_cs<W>(ubase, u0 + 32 + lane, xb);
 
-    for (unsigned long long s = s0; s < s1; ++s) {
-      uint32_t T[W];
+    // SB slabs per pass: their shuffled words stay in registers while every uniform
+    // operand of the item is applied to them; a batch = GX uniform operands x SB slabs
+    for (unsigned long long s = s0; s < s1; s += SB) {
+      uint32_t T[SB][W], Teps[SB], tk[SB][W][MAXK];
+      bool lane_ok[SB];
 #pragma unroll
-      for (int q = 0; q < W; ++q) T[q] = p.tarena[(slab_base + s) * NW + q * 32 + lane];
-      const uint32_t Teps = __shfl_sync(kFull, T[0], 0);
-      uint32_t tk[W][MAXK];
+      for (int j = 0; j < SB; ++j) {
+        const bool slab_ok = s + j < s1;  // warp-uniform
+        lane_ok[j] = slab_ok && (s + j) * 32 + lane < ns;
 #pragma unroll
-      for (int q = 0; q < W; ++q) {
+        for (int q = 0; q < W; ++q) T[j][q] = slab_ok ? p.tarena[(slab_base + s + j) * NW + q * 32 + lane] : 0u;
+        Teps[j] = __shfl_sync(kFull, T[j][0], 0);
 #pragma unroll
-        for (int k = 0; k < MAXK; ++k) {
-          const uint32_t src = s_src[k * NW + q * 32 + lane];
-          const uint32_t t0 = __shfl_sync(kFull, T[0], src & 31);
-          if (W == 2) {
-            const uint32_t t1 = __shfl_sync(kFull, T[W - 1], src & 31);
-            tk[q][k] = (src >> 5) ? t1 : t0;
-          } else {
-            tk[q][k] = t0;
+        for (int q = 0; q < W; ++q) {
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) {
+            const uint32_t src = s_src[k * NW + q * 32 + lane];
+            const uint32_t t0 = __shfl_sync(kFull, T[j][0], src & 31);
+            if (W == 2) {
+              const uint32_t t1 = __shfl_sync(kFull, T[j][W - 1], src & 31);
+              tk[j][q][k] = (src >> 5) ? t1 : t0;
+            } else {
+              tk[j][q][k] = t0;
+            }
           }
         }
       }
-      const unsigned long long sj = s * 32 + lane;
-      const bool lane_ok = sj < ns;
 
-      // one batch of G groups; FULL batches need no per-group bounds test
+      // one batch of GX uniform operands x SB slabs; FULL batches need no operand bound test
       auto batch = [&](uint32_t ub, auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
         uint32_t cs[G][W];
         bool valid[G], skip[G];
-        uint32_t xs[W];  // G divides 32: a batch never straddles the two halves
+        uint32_t xs[W];  // GX divides 32: a batch never straddles the two halves
 #pragma unroll
         for (int q = 0; q < W; ++q) xs[q] = ub >= 32 ? xb[q] : xa[q];
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const uint32_t ui = ub + g;
+        for (int gx = 0; gx < GX; ++gx) {
+          const uint32_t ui = ub + gx;
           uint32_t x[W];
 #pragma unroll
           for (int q = 0; q < W; ++q) x[q] = __shfl_sync(kFull, xs[q], ui & 31);
-          uint32_t acc[W];
+          // enable masks of this operand (all-ones / zero), shared by the SB slabs:
+          // epsilon splits (x[eps] -> T[w], x[w] -> T[eps]) and the proper splits
+          const uint32_t me = (x[0] & 1u) ? kFull : 0u;
+          uint32_t mw[W], mk[W][MAXK];
 #pragma unroll
           for (int q = 0; q < W; ++q) {
-            acc[q] = ((x[0] & 1u) ? T[q] : 0u) | ((x[q] & lanebit) ? Teps : 0u);
+            mw[q] = (x[q] & lanebit) ? kFull : 0u;
 #pragma unroll
-            for (int k = 0; k < MAXK; ++k) {
-              const uint32_t hit = (x[0] & mlo[q][k]) | (W == 2 ? (x[W - 1] & mhi[q][k]) : 0u);
-              acc[q] |= hit ? tk[q][k] : 0u;
-            }
+            for (int k = 0; k < MAXK; ++k)
+              mk[q][k] = ((x[0] & mlo[q][k]) | (W == 2 ? (x[W - 1] & mhi[q][k]) : 0u)) ? kFull : 0u;
           }
 #pragma unroll
-          for (int q = 0; q < W; ++q) cs[g][q] = tr(acc[q]);
-          valid[g] = FULL ? lane_ok : (lane_ok && ui < nu_item);
-          skip[g] = cs_equal<W>(cs[g], x);  // (an x.y == y filter measured slower: see DESIGN.md)
+          for (int j = 0; j < SB; ++j) {
+            const int g = gx * SB + j;
+#pragma unroll
+            for (int q = 0; q < W; ++q) {
+              uint32_t acc = (me & T[j][q]) | (mw[q] & Teps[j]);
+#pragma unroll
+              for (int k = 0; k < MAXK; ++k) acc |= mk[q][k] & tk[j][q][k];
+              cs[g][q] = tr(acc);
+            }
+            valid[g] = FULL ? lane_ok[j] : (lane_ok[j] && ui < nu_item);
+            skip[g] = cs_equal<W>(cs[g], x);  // (an x.y == y filter measured slower: see DESIGN.md)
+          }
         }
-        evaluated += lane_ok ? min((uint32_t)G, nu_item - ub) : 0u;
         process_batch<W, G>(p, cs, valid, skip, [&](int g) {
-          const unsigned long long ui = u0 + ub + g;
+          const unsigned long long ui = u0 + ub + g / SB;
+          const unsigned long long sj = (s + g % SB) * 32 + lane;
           return cand_off + (SLICE_A ? sj * nb + ui : ui * nb + sj);
         }, W == 2 ? &stage : nullptr);
       };
       uint32_t ub = 0;
-      for (; ub + G <= nu_item; ub += G) batch(ub, std::true_type{});
+      for (; ub + GX <= nu_item; ub += GX) batch(ub, std::true_type{});
       if (ub < nu_item) batch(ub, std::false_type{});
+#pragma unroll
+      for (int j = 0; j < SB; ++j) evaluated += lane_ok[j] ? nu_item : 0u;  // every operand of the item
     }
     const uint32_t tot = __reduce_add_sync(kFull, evaluated);
     if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
@@ -1117,7 +1153,8 @@ __global__ void k_rehash(LevelParams p, unsigned long long base, unsigned long l
     uint32_t x[W];
     load_cs<W>(p.arena, t, x);
     if (p.dedup.mode == DEDUP_BITMAP) {
-      atomicOr(&p.dedup.bitmap[x[0] >> 5], 1u << (x[0] & 31));
+      const uint32_t pos = bm_pos(x[0], p.n);
+      atomicOr(&p.dedup.bitmap[pos >> 5], 1u << (pos & 31));
     } else if (p.dedup.mode == DEDUP_HASH64) {
       const unsigned long long key = key64<W>(x);
       const unsigned long long s = hash_cs<W>(x) & p.dedup.mask;
@@ -1217,10 +1254,14 @@ size_t pair_smem(const LevelParams& p, int W) {
 
 template <int W, int MAXK, bool SA>
 int launch_concat_fast_t(const LevelParams& p, cudaStream_t st) {
+  // (one-word CSs append directly: no per-warp stage, more of the SM's L1 for probes)
   const size_t smem = p.nblocks * sizeof(Block) + (size_t)MAXK * 32 * W * 4 +
-                      (size_t)kWarps * kStage * (W * 4 + 8);
+                      (W == 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#ifdef REI_CARVEOUT
+  cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributePreferredSharedMemoryCarveout, REI_CARVEOUT);
+#endif
   const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
   k_concat_fast<W, MAXK, SA><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
@@ -1261,6 +1302,9 @@ int launch_union_sh(const LevelParams& p, cudaStream_t st) {
   const size_t smem = p.nblocks * sizeof(Block) + (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_union<W, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#ifdef REI_CARVEOUT
+  cudaFuncSetAttribute(k_union<W, SH>, cudaFuncAttributePreferredSharedMemoryCarveout, REI_CARVEOUT);
+#endif
   const int grid = grid_for(k_union<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
   k_union<W, SH><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;

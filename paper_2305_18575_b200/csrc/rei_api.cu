@@ -17,6 +17,7 @@
 #include <chrono>
 #include <thread>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -195,19 +196,33 @@ struct Ctx {
   size_t ev_next = 0;
   std::vector<EventPair> pending;
 
+  // device buffers come from the process-wide pool (devmem.cu) unless they are
+  // exported through CUDA IPC (sharded-cache contexts); pinned host blocks are cached
+  cudaError_t dmalloc(void** p, size_t bytes) {
+    if (sharded) return cudaMalloc(p, bytes);
+    return dev_alloc(p, bytes, stream);
+  }
+  template <class T>
+  cudaError_t dmalloc(T** p, size_t bytes) { return dmalloc(reinterpret_cast<void**>(p), bytes); }
+  void dfree(void* p) {
+    if (!p) return;
+    if (sharded) cudaFree(p); else dev_free(p, stream);
+  }
+
   ~Ctx() {
     if (stream) cudaStreamSynchronize(stream);
-    cudaFree(arena); cudaFree(bp); cudaFree(tarena); cudaFree(bitmap); cudaFree(table);
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
-    cudaFree(special); cudaFree(ctl_base); cudaFree(d_blocks); cudaFree(d_peers);
-    if (h_peers) cudaFreeHost(h_peers);
-    cudaFree(tab.split); cudaFree(tab.nsplit); cudaFree(tab.word_len); cudaFree(tab.seeds);
-    if (h_ctl) cudaFreeHost(h_ctl);
-    if (h_blocks) cudaFreeHost(h_blocks);
+    for (void* q : {(void*)arena, (void*)bp, (void*)tarena, (void*)bitmap, (void*)table, (void*)special,
+                    (void*)ctl_base, (void*)d_blocks, (void*)d_peers, (void*)tab.split, (void*)tab.nsplit,
+                    (void*)tab.word_len, (void*)tab.seeds, (void*)d_ctl_all, (void*)g_cs, (void*)g_bp})
+      dfree(q);
+    host_free(h_peers);
+    host_free(h_ctl);
+    host_free(h_blocks);
     for (auto e : ev_pool) cudaEventDestroy(e);
-    cudaFree(d_ctl_all); cudaFree(g_cs); cudaFree(g_bp);
     free_merge_scratch(merge);
     if (nccl) nccl_api().CommDestroy((ncclComm_t)nccl);
+    if (stream) cudaStreamSynchronize(stream);  // the pooled frees above are stream-ordered
     for (int i = 0; i < 3; ++i) {
       if (aux[i]) cudaStreamDestroy(aux[i]);
       if (ev_join[i]) cudaEventDestroy(ev_join[i]);
@@ -281,9 +296,9 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
   uint32_t* a = nullptr;
   unsigned long long* b = nullptr;
   uint32_t* t = nullptr;
-  CUDA_OK(c, cudaMalloc(&a, new_cap * 4ull * c->W32));
-  CUDA_OK(c, cudaMalloc(&b, new_cap * 8ull));
-  CUDA_OK(c, cudaMalloc(&t, new_slab_cap * 32ull * c->W32 * 4ull));
+  CUDA_OK(c, c->dmalloc(&a, new_cap * 4ull * c->W32));
+  CUDA_OK(c, c->dmalloc(&b, new_cap * 8ull));
+  CUDA_OK(c, c->dmalloc(&t, new_slab_cap * 32ull * c->W32 * 4ull));
   if (keep) {
     CUDA_OK(c, cudaMemcpyAsync(a, c->arena, keep * 4ull * c->W32, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_OK(c, cudaMemcpyAsync(b, c->bp, keep * 8ull, cudaMemcpyDeviceToDevice, c->stream));
@@ -292,7 +307,7 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
     CUDA_OK(c, cudaMemcpyAsync(t, c->tarena, keep_slabs * 32ull * c->W32 * 4ull, cudaMemcpyDeviceToDevice,
                                c->stream));
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
-  cudaFree(c->arena); cudaFree(c->bp); cudaFree(c->tarena);
+  c->dfree(c->arena); c->dfree(c->bp); c->dfree(c->tarena);
   c->arena = a; c->bp = b; c->tarena = t;
   c->cap = new_cap;
   c->slab_cap = new_slab_cap;
@@ -300,9 +315,9 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
     uint64_t want = 1;
     while (want < 2 * new_cap) want <<= 1;
     if (want != c->slots) {
-      cudaFree(c->table);
+      c->dfree(c->table);
       c->table = nullptr;
-      CUDA_OK(c, cudaMalloc(&c->table, want * 8ull));
+      CUDA_OK(c, c->dmalloc(&c->table, want * 8ull));
       c->slots = want;
     }
   }
@@ -645,13 +660,13 @@ rei_status gather_ctl(Comm& g, std::vector<LevelCtl>& all) {
 
 rei_status ensure_gather(Ctx* c, uint64_t m) {
   if (c->gather_cap >= m) return REI_OK;
-  cudaFree(c->g_cs);
-  cudaFree(c->g_bp);
+  c->dfree(c->g_cs);
+  c->dfree(c->g_bp);
   c->g_cs = nullptr;
   c->g_bp = nullptr;
   const uint64_t cap = std::max<uint64_t>(m, 2 * c->gather_cap);
-  CUDA_OK(c, cudaMalloc(&c->g_cs, cap * 4ull * c->W32));
-  CUDA_OK(c, cudaMalloc(&c->g_bp, cap * 8ull));
+  CUDA_OK(c, c->dmalloc(&c->g_cs, cap * 4ull * c->W32));
+  CUDA_OK(c, c->dmalloc(&c->g_bp, cap * 8ull));
   c->gather_cap = cap;
   return REI_OK;
 }
@@ -755,7 +770,7 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   };
   // fork: the level's kernels are independent (they read lower levels and insert
   // through atomics), so ? / * (and union) may run on auxiliary streams
-  const int conc = c->concurrency;
+  const int conc = std::min(3, c->concurrency);
   cudaStream_t su = conc >= 1 ? c->aux[0] : c->stream;
   cudaStream_t sn = conc >= 2 ? c->aux[1] : c->stream;
   cudaStream_t sc = conc >= 3 ? c->aux[2] : c->stream;
@@ -904,6 +919,8 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
 
   std::vector<Block> cat, uni;
   std::vector<LevelCtl> all;
+  const bool trace = getenv("REI_TRACE") != nullptr;
+  auto t_level = std::chrono::steady_clock::now();
   for (int cost = c1 + 1; cost <= (int)max_cost; ++cost) {
     if (c0->otf_level && needs_uncached(c0, cost)) {
       // OnTheFly mode needs a level it did not cache: stop
@@ -974,6 +991,12 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
           if ((s = rebuild_dedup(c, c->arena_used)) != REI_OK) return s;  // drop partial inserts
         }
       }
+    }
+    if (trace) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[rei_solve] level %3d host %8.3f ms device %8.3f ms\n", cost,
+              std::chrono::duration<double, std::milli>(now - t_level).count(), level_ms);
+      t_level = now;
     }
     const bool otf_now = c0->otf_level != 0;
     uint64_t found_rank = ~0ull, evaluated = 0, eval_c = 0, eval_u = 0;
@@ -1559,6 +1582,14 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   g_init_error.clear();
   if (!out || !alphabet) { g_init_error = "null argument"; return REI_EINVAL; }
   *out = nullptr;
+  // REI_TRACE=1: host wall-clock of the init phases on stderr (diagnostics only)
+  const bool trace = getenv("REI_TRACE") != nullptr;
+  const auto t_start = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (trace)
+      fprintf(stderr, "[rei_init] %-28s %8.3f ms\n", what,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
   auto c = std::make_unique<Ctx>();
   c->alphabet = alphabet;
   const size_t k = c->alphabet.size();
@@ -1648,33 +1679,39 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     c->own_stream = true;
   }
   auto fail = [&](const std::string& m) { g_init_error = m; return REI_ECUDA; };
+  phase("validate + stream");
   {
     const char* ev = getenv("REI_CONCURRENT");
-    c->concurrency = ev ? std::max(0, std::min(3, atoi(ev))) : 3;
-    if (c->concurrency >= 1) {
+    c->concurrency = ev ? std::max(0, std::min(4, atoi(ev))) : 3;
+    // 3: concat on a high-priority stream, union on a low-priority one; 4: the reverse
+    // (union candidates are the cheaper ones: with an early exit, cheapest first)
+    const int nstreams = std::min(3, c->concurrency);
+    if (nstreams >= 1) {
       int prio_lo = 0, prio_hi = 0;
       cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-      for (int i = 0; i < c->concurrency; ++i)
-        if (cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking,
-                                         i == 1 && c->concurrency >= 3 ? prio_lo : prio_hi) != cudaSuccess ||
+      const int low = c->concurrency == 3 ? 1 : c->concurrency == 4 ? 2 : -1;
+      for (int i = 0; i < nstreams; ++i)
+        if (cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking, i == low ? prio_lo : prio_hi) !=
+                cudaSuccess ||
             cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
           return fail("auxiliary stream creation failed");
       if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return fail("event creation failed");
     }
   }
-  if (cudaMalloc(&c->tab.split, sizeof(uint32_t) * kMaxSplitRows * kMaxNW) != cudaSuccess ||
-      cudaMalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
-      cudaMalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
-      cudaMalloc(&c->tab.seeds, sizeof(uint32_t) * kMaxW32 * k) != cudaSuccess ||
-      cudaMalloc(&c->ctl_base, 2 * sizeof(LevelCtl)) != cudaSuccess ||
-      cudaMalloc(&c->d_peers, sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
-      cudaMallocHost(&c->h_peers, sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
-      cudaMalloc(&c->special, sizeof(unsigned int)) != cudaSuccess ||
-      cudaMalloc(&c->d_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess ||
-      cudaMallocHost(&c->h_ctl, sizeof(LevelCtl)) != cudaSuccess ||
-      cudaMallocHost(&c->h_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess)
+  if (c->dmalloc(&c->tab.split, sizeof(uint32_t) * kMaxSplitRows * kMaxNW) != cudaSuccess ||
+      c->dmalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
+      c->dmalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
+      c->dmalloc(&c->tab.seeds, sizeof(uint32_t) * kMaxW32 * k) != cudaSuccess ||
+      c->dmalloc(&c->ctl_base, 2 * sizeof(LevelCtl)) != cudaSuccess ||
+      c->dmalloc(&c->d_peers, sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
+      host_alloc(reinterpret_cast<void**>(&c->h_peers), sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
+      c->dmalloc(&c->special, sizeof(unsigned int)) != cudaSuccess ||
+      c->dmalloc(&c->d_blocks, sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess ||
+      host_alloc(reinterpret_cast<void**>(&c->h_ctl), sizeof(LevelCtl)) != cudaSuccess ||
+      host_alloc(reinterpret_cast<void**>(&c->h_blocks), sizeof(Block) * 3 * Ctx::kMaxBlocks) != cudaSuccess)
     return fail(std::string("device allocation failed: ") + cudaGetErrorString(cudaGetLastError()));
+  phase("aux streams + small buffers");
   c->ctl = c->ctl_base;
   cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
   if (c->world > 1 && !c->sharded) {  // one process per GPU: the level exchange runs over NCCL (collective)
@@ -1686,7 +1723,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       return REI_ENCCL;
     }
     c->nccl = comm;
-    if (cudaMalloc(&c->d_ctl_all, sizeof(LevelCtl) * c->world) != cudaSuccess)
+    if (c->dmalloc(&c->d_ctl_all, sizeof(LevelCtl) * c->world) != cudaSuccess)
       return fail("device allocation failed (control lines)");
   }
   if (c->P.empty() && c->N.empty()) {
@@ -1701,6 +1738,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     return err.find("|IC|") != std::string::npos || err.find("splits") != std::string::npos ? REI_EINVAL
                                                                                               : REI_ECUDA;
   }
+  phase("device precompute");
   for (auto& w : c->P) c->h2d_bytes += w.size() + 4;
   for (auto& w : c->N) c->h2d_bytes += w.size() + 4;
   c->d2h_bytes += 64 + 8ull * c->tab.n;  // table summary + IC keys
@@ -1709,11 +1747,12 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   if (!c->budget) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
+    if (!c->sharded) fr += dev_pool_idle_bytes(c->device);  // blocks the pool keeps for reuse
     c->budget = (uint64_t)(0.8 * (double)fr);
   }
   if (c->mode == DEDUP_BITMAP) {
     c->bitmap_words = std::max<uint64_t>(1, (1ull << c->tab.n) / 32);
-    if (cudaMalloc(&c->bitmap, c->bitmap_words * 4) != cudaSuccess) return fail("bitmap allocation failed");
+    if (c->dmalloc(&c->bitmap, c->bitmap_words * 4) != cudaSuccess) return fail("bitmap allocation failed");
     c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
   }
   // bitmap mode: at most 2^n distinct CSs exist, so reserve them all up front (up to
@@ -1729,6 +1768,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   }
   if (alloc_arena(c.get(), cap0, 0, 0) != REI_OK) return fail(c->err);
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail("init sync failed");
+  phase("dedup set + language cache");
   if (c->sharded && c->world > 1) {  // collective: map every rank's buffers (CUDA IPC)
     rei_status st = link_ipc(c.get());
     if (st != REI_OK) { g_init_error = c->err; return st; }
@@ -1798,6 +1838,8 @@ const char* rei_last_error(const void* ctx) {
 const char* rei_last_init_error(void) { return rei::g_init_error.c_str(); }
 
 void rei_destroy(void* ctx) { delete static_cast<Ctx*>(ctx); }
+
+void rei_release_cached_memory(void) { rei::release_cached_memory(); }
 
 rei_status rei_ic(const void* ctx, uint32_t k, char* buf, size_t cap, uint32_t* n_ic) {
   if (!ctx) return REI_EINVAL;

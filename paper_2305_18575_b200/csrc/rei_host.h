@@ -50,6 +50,15 @@ void free_merge_scratch(MergeScratch& s);
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                uint64_t count, cudaStream_t st);
 
+// Process-wide caching allocators (devmem.cu): pooled stream-ordered device memory,
+// cached pinned host blocks.
+cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
+void dev_free(void* p, cudaStream_t st);
+uint64_t dev_pool_idle_bytes(int dev);
+cudaError_t host_alloc(void** p, size_t bytes);
+void host_free(void* p);
+void release_cached_memory();
+
 // Work-item tiling of the pair kernels (uniform operands x slabs of 32).
 constexpr int kTileU = 64;    // uniform operands per work item
 constexpr int kTileS = 4;     // slabs (of 32 sliced operands) per work item

@@ -130,6 +130,8 @@ def load_library():
     lib.rei_last_error.argtypes = [vp]
     lib.rei_last_init_error.restype = c.c_char_p
     lib.rei_destroy.argtypes = [vp]
+    lib.rei_release_cached_memory.argtypes = []
+    lib.rei_release_cached_memory.restype = None
     lib.rei_ic.restype = c.c_int
     lib.rei_ic.argtypes = [vp, c.c_uint32, c.c_char_p, c.c_size_t, c.POINTER(c.c_uint32)]
     lib.rei_splits.restype = c.c_int
@@ -187,6 +189,12 @@ class Result:
     n_ic: int
     cs_words: int
     levels: List[LevelStat]
+
+
+def release_cached_memory() -> None:
+    """Return the device / pinned blocks that destroyed contexts left in the
+    library's caches to the driver (rei_release_cached_memory)."""
+    load_library().rei_release_cached_memory()
 
 
 def _strs(xs: Sequence[str]):

@@ -48,10 +48,17 @@ def main():
     libs = {"base": os.path.join(PKG, "librei_b200.so")}
     for f in sorted(glob.glob(os.path.join(PKG, "librei_b200_*.so"))):
         libs[os.path.basename(f)[len("librei_b200_"):-3]] = f
-    res = {k: [] for k in libs}
+    modes = [m for m in os.environ.get("AB_CONC", "").split(",") if m]  # REI_CONCURRENT modes
+    runs_of = {}
+    for name, path in libs.items():
+        for m in modes or [None]:
+            runs_of[name if m is None else f"{name}/c{m}"] = (path, m)
+    res = {k: [] for k in runs_of}
     for rnd in range(2):
-        for name, path in libs.items():
+        for name, (path, m) in runs_of.items():
             env = dict(os.environ, REI_LIB=path)
+            if m is not None:
+                env["REI_CONCURRENT"] = m
             out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, workload, reps)], env=env,
                                  capture_output=True, text=True, timeout=600)
             if out.returncode != 0:
