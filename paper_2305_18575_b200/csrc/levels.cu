@@ -403,7 +403,11 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
       for (int g = 0; g < G; ++g) {
         const bool need = valid[g] && !skip[g];
         pos[g] = bm_pos(cs[g][0], p.n);
+#ifdef REI_PROBE_CG  // (A/B) probe through L2 only
+        word[g] = need ? __ldcg(&p.dedup.bitmap[pos[g] >> 5]) : kFull;
+#else
         word[g] = need ? p.dedup.bitmap[pos[g] >> 5] : kFull;
+#endif
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
@@ -477,7 +481,13 @@ struct TransposeLane {
     // byte-permute selectors of the 16- and 8-bit stages ({partner:own}, own = bytes 0-3)
     rot[0] = (lane & 16) ? 0x3276u : 0x5410u;
     rot[1] = (lane & 8) ? 0x3715u : 0x6240u;
+    // paired byte stages: {send, receive into b} selectors (receive into a = rot[])
+    psel[0] = (lane & 16) ? 0x5410u : 0x3276u;
+    psel[1] = (lane & 16) ? 0x3254u : 0x7610u;
+    psel[2] = (lane & 8) ? 0x6240u : 0x3715u;
+    psel[3] = (lane & 8) ? 0x3614u : 0x7250u;
   }
+  uint32_t psel[4];
   // Same matrix transpose as transpose32(): the 16- and 8-bit stages move whole bytes
   // (one PRMT each, per-lane selector), the 4/2/1-bit stages rotate + merge (SHF, LOP3).
   __device__ __forceinline__ uint32_t operator()(uint32_t x) const {
@@ -493,6 +503,84 @@ struct TransposeLane {
       x = (x & km[s]) | (yr & ~km[s]);
     }
     return x;
+  }
+  // Two transposes at once (a, b): every butterfly stage moves half of each word to
+  // the partner lane, so the two outgoing halves share ONE shuffle (packed), trading
+  // one SHFL (an L1TEX wavefront) for one ALU op per stage.
+  __device__ __forceinline__ void pair(uint32_t& a, uint32_t& b) const {
+    // 16- and 8-bit stages: byte permutes
+    uint32_t y = __shfl_xor_sync(kFull, __byte_perm(a, b, psel[0]), 16);
+    b = __byte_perm(b, y, psel[1]);
+    a = __byte_perm(a, y, rot[0]);
+    y = __shfl_xor_sync(kFull, __byte_perm(a, b, psel[2]), 8);
+    b = __byte_perm(b, y, psel[3]);
+    a = __byte_perm(a, y, rot[1]);
+    // 4-, 2-, 1-bit stages: the lane keeps km, sends a's other bits in place and b's
+    // rotated into the km positions
+#pragma unroll
+    for (int s = 2; s < 5; ++s) {
+      const uint32_t pk = (a & ~km[s]) | (__funnelshift_r(b, b, rot[s]) & km[s]);
+      y = __shfl_xor_sync(kFull, pk, 16u >> s);
+      b = (b & km[s]) | (y & ~km[s]);
+      a = (a & km[s]) | (__funnelshift_l(y, y, rot[s]) & ~km[s]);
+    }
+  }
+};
+
+// Skewed 32x32 bit-matrix transpose with warp-uniform masks (no per-lane constants
+// but the shuffle sources).  Element (row w, column t) of the matrix (lane w holds row
+// w) is first placed at bit k = (w - t) mod 32 of lane w by the pre-skew
+// z_w = rotr(brev(row_w), 31 - w); stage i then moves every bit whose position has bit
+// i set down by 2^i lanes (one SHFL + one LOP3 with an immediate mask), so the element
+// ends in lane w - k = t at position k = w - t, and a rotate-left by t puts row w's bit
+// at position w.  The pre-skew is a bit permutation, so it commutes with the AND/OR of
+// the fold against all-ones / zero masks: it is applied to the slab terms once per
+// slab, not per candidate.  Per transpose: 5 SHFL + 5 LOP3 + 1 SHF.
+struct SkewTranspose {
+  uint32_t src[5];  // lane + 16, 8, 4, 2, 1 (mod 32: SHFL wraps)
+  uint32_t lane;
+  __device__ __forceinline__ explicit SkewTranspose(uint32_t l) : lane(l) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) src[i] = (l + (16u >> i)) & 31u;
+  }
+  __device__ __forceinline__ uint32_t pre(uint32_t v) const {
+    const uint32_t r = __brev(v);
+    return __funnelshift_r(r, r, 31u - lane);
+  }
+  __device__ __forceinline__ uint32_t operator()(uint32_t z) const {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      const uint32_t j = 16u >> i;
+      const uint32_t M = (j == 16) ? 0xFFFF0000u : (j == 8) ? 0xFF00FF00u
+                       : (j == 4) ? 0xF0F0F0F0u : (j == 2) ? 0xCCCCCCCCu : 0xAAAAAAAAu;
+      const uint32_t y = __shfl_sync(kFull, z, src[i]);
+      // z = (z & ~M) | (y & M) as ONE lop3 (truth table 0xB8 for a=z, b=M, c=y; the
+      // compiler otherwise splits it in two)
+      asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(z) : "r"(z), "r"(M), "r"(y));
+    }
+    return __funnelshift_l(z, z, lane);
+  }
+  // Two transposes (a, b): the byte-granular stages (16, 8) carry both words' moving
+  // bytes in ONE shuffle (byte permutes with warp-uniform selectors), trading one SHFL
+  // for one ALU op each; the bit stages stay single.
+  __device__ __forceinline__ void pair(uint32_t& a, uint32_t& b) const {
+    uint32_t y = __shfl_sync(kFull, __byte_perm(a, b, 0x3276u), src[0]);
+    a = __byte_perm(a, y, 0x7610u);
+    b = __byte_perm(b, y, 0x5410u);
+    y = __shfl_sync(kFull, __byte_perm(a, b, 0x3715u), src[1]);
+    a = __byte_perm(a, y, 0x7250u);
+    b = __byte_perm(b, y, 0x6240u);
+#pragma unroll
+    for (int i = 2; i < 5; ++i) {
+      const uint32_t j = 16u >> i;
+      const uint32_t M = (j == 4) ? 0xF0F0F0F0u : (j == 2) ? 0xCCCCCCCCu : 0xAAAAAAAAu;
+      const uint32_t ya = __shfl_sync(kFull, a, src[i]);
+      const uint32_t yb = __shfl_sync(kFull, b, src[i]);
+      asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(a) : "r"(a), "r"(M), "r"(ya));
+      asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(b) : "r"(b), "r"(M), "r"(yb));
+    }
+    a = __funnelshift_l(a, a, lane);
+    b = __funnelshift_l(b, b, lane);
   }
 };
 
@@ -681,7 +769,13 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 
   const uint32_t lane = lane_id();
   const uint32_t lanebit = 1u << lane;
+#ifdef REI_TRANSPOSE_BFLY  // (A/B) the butterfly with per-lane masks / rotations
   const TransposeLane tr(lane);
+  auto pre = [](uint32_t v) { return v; };
+#else
+  const SkewTranspose tr(lane);
+  auto pre = [&](uint32_t v) { return tr.pre(v); };
+#endif
   // this warp's stage for new CSs (after the split table): [kWarps][kStage][W] + ranks
   WarpStage<W> stage;
   {
@@ -759,11 +853,22 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
           }
         }
       }
+      // the slab terms in the transposer's input layout (a per-lane bit permutation)
+#pragma unroll
+      for (int j = 0; j < SB; ++j) {
+        Teps[j] = pre(Teps[j]);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          T[j][q] = pre(T[j][q]);
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k) tk[j][q][k] = pre(tk[j][q][k]);
+        }
+      }
 
       // one batch of GX uniform operands x SB slabs; FULL batches need no operand bound test
       auto batch = [&](uint32_t ub, auto full_tag) {
         constexpr bool FULL = decltype(full_tag)::value;
-        uint32_t cs[G][W];
+        uint32_t cs[G][W], xk[GX][W];
         bool valid[G], skip[G];
         uint32_t xs[W];  // GX divides 32: a batch never straddles the two halves
 #pragma unroll
@@ -793,12 +898,28 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
               uint32_t acc = (me & T[j][q]) | (mw[q] & Teps[j]);
 #pragma unroll
               for (int k = 0; k < MAXK; ++k) acc |= mk[q][k] & tk[j][q][k];
-              cs[g][q] = tr(acc);
+              cs[g][q] = acc;  // bit-slice; transposed below
             }
             valid[g] = FULL ? lane_ok[j] : (lane_ok[j] && ui < nu_item);
-            skip[g] = cs_equal<W>(cs[g], x);  // (an x.y == y filter measured slower: see DESIGN.md)
           }
+#pragma unroll
+          for (int q = 0; q < W; ++q) xk[gx][q] = x[q];
         }
+        // slices -> candidate CSs (one per lane)
+        {
+          uint32_t* v = &cs[0][0];
+#if !defined(REI_TRANSPOSE_SINGLE)  // (A/B on B200: skew pairs 2 % faster than single; butterfly pairs were 5 % slower)
+#pragma unroll
+          for (int i = 0; i + 1 < G * W; i += 2) tr.pair(v[i], v[i + 1]);
+          if ((G * W) & 1) v[G * W - 1] = tr(v[G * W - 1]);
+#else
+#pragma unroll
+          for (int i = 0; i < G * W; ++i) v[i] = tr(v[i]);
+#endif
+        }
+        // equals its uniform operand: cached (an x.y == y filter measured slower: DESIGN.md)
+#pragma unroll
+        for (int g = 0; g < G; ++g) skip[g] = cs_equal<W>(cs[g], xk[g / SB]);
         process_batch<W, G>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u0 + ub + g / SB;
           const unsigned long long sj = (s + g % SB) * 32 + lane;
