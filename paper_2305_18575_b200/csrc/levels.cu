@@ -947,7 +947,7 @@ template <int W, bool SH = false>
 #ifndef REI_UNION_G1
 #define REI_UNION_G1 4
 #endif
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : 1) k_union(LevelParams p) {
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : 1)) k_union(LevelParams p) {  // (minB: W = 2 keeps 2 CTAs per SM)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
@@ -995,44 +995,44 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : 1) k_u
       if (lane + 32 < nu_item) load_cs<W>(p.arena, u_base + u0 + 32 + lane, xb);
     }
 
-    for (unsigned long long s = s0; s < s1; ++s) {
-      const unsigned long long sj = s * 32 + lane;
-      const bool lane_ok = sj < ns;
-      uint32_t y[W];
-      if (lane_ok) load_cs<W>(p.arena, s_base + sj, y);
-      else {
+    // G slabs per pass (one operand of the sliced level per lane and slab): each uniform
+    // operand is broadcast once and applied to all G of them (a batch = G candidates)
+    for (unsigned long long s = s0; s < s1; s += G) {
+      const unsigned long long s_last = min(s + G, s1) - 1;
+      uint32_t y[G][W];
+      bool lane_ok[G];
 #pragma unroll
-        for (int q = 0; q < W; ++q) y[q] = 0;
+      for (int j = 0; j < G; ++j) {
+        const unsigned long long sj = (s + j) * 32 + lane;
+        lane_ok[j] = s + j < s1 && sj < ns;
+        if (lane_ok[j]) load_cs<W>(p.arena, s_base + sj, y[j]);
+        else {
+#pragma unroll
+          for (int q = 0; q < W; ++q) y[j][q] = 0;
+        }
       }
-      for (uint32_t ub = 0; ub < nu_item; ub += G) {
-        if (tri && u0 + ub >= s * 32 + 31) break;  // no j > i left in this slab
+      for (uint32_t ub = 0; ub < nu_item; ++ub) {
+        if (tri && u0 + ub >= s_last * 32 + 31) break;  // no j > i left in these slabs
+        uint32_t x[W];
+        if (W <= 2) {
+#pragma unroll
+          for (int q = 0; q < W; ++q) x[q] = __shfl_sync(kFull, ub >= 32 ? xb[q] : xa[q], ub & 31);
+        } else {
+          load_cs<W>(p.arena, u_base + u0 + ub, x);
+        }
         uint32_t cs[G][W];
         bool valid[G], skip[G];
-        const bool hi_half = ub >= 32;
-        uint32_t nvalid = 0;
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-          const uint32_t ui = ub + g;
-          const bool active = ui < nu_item;
-          uint32_t x[W];
-          if (W <= 2) {
+        for (int j = 0; j < G; ++j) {
 #pragma unroll
-            for (int q = 0; q < W; ++q) x[q] = __shfl_sync(kFull, hi_half ? xb[q] : xa[q], ui & 31);
-          } else if (active) {
-            load_cs<W>(p.arena, u_base + u0 + ui, x);
-          } else {
-#pragma unroll
-            for (int q = 0; q < W; ++q) x[q] = 0;
-          }
-#pragma unroll
-          for (int q = 0; q < W; ++q) cs[g][q] = x[q] | y[q];
-          valid[g] = active && lane_ok && (!tri || sj > u0 + ui);
-          skip[g] = cs_equal<W>(cs[g], x) || cs_equal<W>(cs[g], y);
-          nvalid += valid[g] ? 1u : 0u;
+          for (int q = 0; q < W; ++q) cs[j][q] = x[q] | y[j][q];
+          valid[j] = lane_ok[j] && (!tri || (s + j) * 32 + lane > u0 + ub);
+          skip[j] = cs_equal<W>(cs[j], x) || cs_equal<W>(cs[j], y[j]);
+          evaluated += valid[j] ? 1u : 0u;
         }
-        evaluated += nvalid;
         process_batch<W, G, SH>(p, cs, valid, skip, [&](int g) {
-          const unsigned long long ui = u0 + ub + g;
+          const unsigned long long ui = u0 + ub;
+          const unsigned long long sj = (s + g) * 32 + lane;
           const unsigned long long i = slice_a ? sj : ui;
           const unsigned long long j = slice_a ? ui : sj;
           return cand_off + (tri ? i * na - i * (i + 1) / 2 + (j - i - 1) : i * nb + j);
