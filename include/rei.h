@@ -160,11 +160,12 @@ rei_status rei_transfer_bytes(const void* ctx, uint64_t* h2d, uint64_t* d2h);
 
 const char* rei_last_error(const void* ctx);
 const char* rei_last_init_error(void);
-/* rei_destroy frees the context.  Its device buffers return to a process-wide pool
- * (one cudaMemPool per device, freed blocks kept mapped) and its pinned host blocks to
- * a free list, so the next rei_init in the process reuses them instead of paying
- * cudaMalloc / cudaMallocHost again (sharded-cache contexts use plain cudaMalloc: their
- * buffers are exported through CUDA IPC). */
+/* rei_destroy frees the context.  Its device buffers return to a process-wide cache
+ * (per device, size-keyed free lists of cudaMalloc blocks, kept mapped) and its pinned
+ * host blocks to a free list, so the next rei_init / growth in the process reuses them
+ * instead of paying cudaMalloc / cudaMallocHost again (sharded-cache contexts use plain
+ * cudaMalloc: their buffers are exported through CUDA IPC).  Idle cached blocks count
+ * as free memory in the default budget and are released when an allocation fails. */
 void rei_destroy(void* ctx);
 /* Return every cached (idle) device and pinned host block to the driver.  Safe at
  * any time; live contexts are unaffected. */

@@ -1,17 +1,22 @@
 // devmem.cu -- process-wide caching allocators of the runtime (memory manager).
 //
-// A context's buffers are large (the bitmap-mode arena of Table 1 row 1 is ~0.5 GB)
-// and a serving process creates many contexts (one per specification, the paper's
-// 5,160-run benchmark suite).  cudaMalloc / cudaMallocHost of fresh
-// memory costs milliseconds per call, so:
-//   * device memory comes from one cudaMemPool per device whose release threshold is
-//     unbounded: blocks freed by rei_destroy stay mapped and are handed to the next
-//     rei_init (stream-ordered: cudaMallocFromPoolAsync / cudaFreeAsync on the
-//     context's stream);
-//   * pinned host blocks (control lines, block tables) come from a size-keyed free
-//     list.
-// rei_release_cached_memory() trims both.  Buffers that are exported through CUDA IPC
-// (sharded-cache contexts) do not use the pool (pool memory needs an IPC-capable pool).
+// A context's buffers are large (the bitmap-mode arena of Table 1 row 1 is ~0.5 GB;
+// a two-word-CS search grows its cache and hash set to tens of GB) and a serving
+// process creates many contexts (one per specification, the paper's 5,160-run
+// benchmark suite).  Fresh device memory costs ~8 ms per GB to map
+// (measured on B200: a 51 GB arena + 34 GB hash set took 0.7 s), and cudaMallocHost
+// costs milliseconds per call, so:
+//   * device blocks freed by a context (rei_destroy, or a grown arena's old buffers)
+//     are kept, per device, in a size-keyed free list and handed to the next request
+//     of the same size class (sizes rounded up to 2 MiB; a cached block up to 1/8
+//     larger than the request is accepted).  A context's growth sequence is
+//     deterministic, so the next context on the same specification reuses every block.
+//     The stream is synchronised before a block enters the list (frees are rare).
+//     On cudaErrorMemoryAllocation the idle blocks of that device are released and
+//     the allocation retried;
+//   * pinned host blocks (control lines, block tables) come from a similar free list.
+// rei_release_cached_memory() releases both.  Sharded-cache contexts export their
+// buffers through CUDA IPC and allocate with plain cudaMalloc (rei_api.cu).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -24,71 +29,85 @@
 namespace rei {
 namespace {
 
-std::mutex g_mu;
-std::map<int, cudaMemPool_t> g_pools;                 // device -> pool
-std::multimap<size_t, void*> g_host_free;             // size -> pinned block
-std::map<void*, size_t> g_host_size;                  // every pinned block we own
+constexpr size_t kGran = size_t(2) << 20;
 
-cudaError_t pool_of(int dev, cudaMemPool_t* out) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_pools.find(dev);
-  if (it != g_pools.end()) {
-    *out = it->second;
-    return cudaSuccess;
+struct DevBlock {
+  int dev;
+  size_t bytes;
+};
+
+std::mutex g_mu;
+std::map<int, std::multimap<size_t, void*>> g_dev_free;  // device -> (size -> idle block)
+std::map<void*, DevBlock> g_dev_blocks;                   // every device block we own
+std::multimap<size_t, void*> g_host_free;                 // size -> idle pinned block
+std::map<void*, size_t> g_host_size;                      // every pinned block we own
+
+size_t round_up(size_t b) { return (b + kGran - 1) / kGran * kGran; }
+
+// Take a cached block of at least `bytes` (<= bytes + bytes/8) on `dev`; nullptr if none.
+void* take_cached(int dev, size_t bytes) {
+  auto& fl = g_dev_free[dev];
+  auto it = fl.lower_bound(bytes);
+  if (it == fl.end() || it->first > bytes + bytes / 8) return nullptr;
+  void* p = it->second;
+  fl.erase(it);
+  return p;
+}
+
+void release_device(int dev) {  // caller holds g_mu
+  auto& fl = g_dev_free[dev];
+  for (auto& kv : fl) {
+    cudaFree(kv.second);
+    g_dev_blocks.erase(kv.second);
   }
-  cudaMemPoolProps props = {};
-  props.allocType = cudaMemAllocationTypePinned;
-  props.handleTypes = cudaMemHandleTypeNone;
-  props.location.type = cudaMemLocationTypeDevice;
-  props.location.id = dev;
-  cudaMemPool_t pool;
-  cudaError_t e = cudaMemPoolCreate(&pool, &props);
-  if (e != cudaSuccess) return e;
-  uint64_t keep = ~0ull;  // never release freed blocks on synchronisation
-  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-  if (e != cudaSuccess) return e;
-  g_pools[dev] = pool;
-  *out = pool;
-  return cudaSuccess;
+  fl.clear();
 }
 
 }  // namespace
 
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+  (void)st;
   *p = nullptr;
-  if (bytes == 0) bytes = 1;
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  cudaMemPool_t pool;
-  if ((e = pool_of(dev, &pool)) != cudaSuccess) return e;
-  e = cudaMallocFromPoolAsync(p, bytes, pool, st);
+  const size_t want = round_up(bytes ? bytes : 1);
+  std::lock_guard<std::mutex> lk(g_mu);
+  if ((*p = take_cached(dev, want)) != nullptr) return cudaSuccess;
+  e = cudaMalloc(p, want);
   if (e == cudaErrorMemoryAllocation) {
-    // the idle blocks the pool keeps may not fit this request: return them and retry
-    cudaGetLastError();
-    cudaStreamSynchronize(st);
-    cudaMemPoolTrimTo(pool, 0);
-    e = cudaMallocFromPoolAsync(p, bytes, pool, st);
+    cudaGetLastError();  // not sticky: clear it, return the idle blocks and retry once
+    release_device(dev);
+    e = cudaMalloc(p, want);
   }
-  return e;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *p = nullptr;
+    return e;
+  }
+  g_dev_blocks[*p] = {dev, want};
+  return cudaSuccess;
 }
 
 void dev_free(void* p, cudaStream_t st) {
-  if (p) cudaFreeAsync(p, st);
+  if (!p) return;
+  cudaStreamSynchronize(st);  // no kernel of this stream may still touch the block
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_dev_blocks.find(p);
+  if (it == g_dev_blocks.end()) {
+    cudaFree(p);
+    return;
+  }
+  g_dev_free[it->second.dev].emplace(it->second.bytes, p);
 }
 
 uint64_t dev_pool_idle_bytes(int dev) {
-  cudaMemPool_t pool;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    auto it = g_pools.find(dev);
-    if (it == g_pools.end()) return 0;
-    pool = it->second;
-  }
-  uint64_t reserved = 0, used = 0;
-  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
-  cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
-  return reserved > used ? reserved - used : 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  uint64_t s = 0;
+  auto it = g_dev_free.find(dev);
+  if (it != g_dev_free.end())
+    for (auto& kv : it->second) s += kv.first;
+  return s;
 }
 
 cudaError_t host_alloc(void** p, size_t bytes) {
@@ -117,19 +136,19 @@ void host_free(void* p) {
 }
 
 void release_cached_memory() {
-  std::vector<void*> host;
-  std::vector<cudaMemPool_t> pools;
-  {
-    std::lock_guard<std::mutex> lk(g_mu);
-    for (auto& kv : g_host_free) {
-      host.push_back(kv.second);
-      g_host_size.erase(kv.second);
-    }
-    g_host_free.clear();
-    for (auto& kv : g_pools) pools.push_back(kv.second);
+  std::lock_guard<std::mutex> lk(g_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto& kv : g_dev_free) {
+    cudaSetDevice(kv.first);
+    release_device(kv.first);
   }
-  for (void* p : host) cudaFreeHost(p);
-  for (cudaMemPool_t pool : pools) cudaMemPoolTrimTo(pool, 0);
+  cudaSetDevice(cur);
+  for (auto& kv : g_host_free) {
+    cudaFreeHost(kv.second);
+    g_host_size.erase(kv.second);
+  }
+  g_host_free.clear();
 }
 
 }  // namespace rei

@@ -226,15 +226,20 @@ __device__ __forceinline__ bool insert_hash64(const S& p, unsigned long long key
   return false;
 }
 
-// Bitmap position of a one-word CS (dedup over all 2^n languages, |IC| <= 32).
-// REI_BITMAP_REV (A/B experiment): bit-reversed, so the long IC words select the
-// word within a 128-byte line and the short ones the line.
+// Bitmap position of a one-word CS (dedup over all 2^n languages, |IC| <= 32): the
+// n-bit CS bit-reversed.  The bits of the long IC words (high CS bits) are the ones
+// that vary most among the 32 candidates of a warp group (one uniform operand x 32
+// consecutive cached operands), so reversed they select the bit within a 32-byte
+// sector and the short-word bits select the sector: a group's probes touch fewer
+// distinct sectors (Table 1 row 1, level-20 groups in the oracle's cache order: 17.3
+// -> 12.7 sectors per 32 probes), and the concat kernel is bound by L1TEX tag lookups
+// (A/B on B200: solve 46.6 -> 39.7 ms).  REI_BITMAP_IDENTITY restores plain order.
 __device__ __forceinline__ uint32_t bm_pos(uint32_t cs, uint32_t n) {
-#ifdef REI_BITMAP_REV
-  return n ? __brev(cs) >> (32 - n) : 0u;
-#else
+#ifdef REI_BITMAP_IDENTITY
   (void)n;
   return cs;
+#else
+  return n ? __brev(cs) >> (32 - n) : 0u;
 #endif
 }
 

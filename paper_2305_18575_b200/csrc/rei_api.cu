@@ -296,9 +296,15 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
   uint32_t* a = nullptr;
   unsigned long long* b = nullptr;
   uint32_t* t = nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   CUDA_OK(c, c->dmalloc(&a, new_cap * 4ull * c->W32));
   CUDA_OK(c, c->dmalloc(&b, new_cap * 8ull));
   CUDA_OK(c, c->dmalloc(&t, new_slab_cap * 32ull * c->W32 * 4ull));
+  if (getenv("REI_TRACE")) {
+    cudaStreamSynchronize(c->stream);
+    fprintf(stderr, "[rei_alloc] arena %llu entries: %.3f ms\n", (unsigned long long)new_cap,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  }
   if (keep) {
     CUDA_OK(c, cudaMemcpyAsync(a, c->arena, keep * 4ull * c->W32, cudaMemcpyDeviceToDevice, c->stream));
     CUDA_OK(c, cudaMemcpyAsync(b, c->bp, keep * 8ull, cudaMemcpyDeviceToDevice, c->stream));
@@ -599,9 +605,21 @@ rei_status grow(Ctx* c, uint64_t need_entries) {
   if (c->mode == DEDUP_BITMAP) nc = std::min<uint64_t>(nc, (1ull << c->tab.n) + 64);
   nc = std::min(nc, max_cap);
   if (nc <= c->cap) return REI_OUT_OF_MEMORY;
+  const bool trace = getenv("REI_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   rei_status s = alloc_arena(c, nc, c->arena_used, c->slabs_used);
   if (s != REI_OK) return s;
-  return rebuild_dedup(c, c->arena_used);
+  const auto t1 = std::chrono::steady_clock::now();
+  s = rebuild_dedup(c, c->arena_used);
+  if (trace) {
+    cudaStreamSynchronize(c->stream);
+    const auto t2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rei_grow] %llu -> %llu entries: realloc+copy %.3f ms, rehash %llu %.3f ms\n",
+            (unsigned long long)c->cap, (unsigned long long)nc,
+            std::chrono::duration<double, std::milli>(t1 - t0).count(), (unsigned long long)c->arena_used,
+            std::chrono::duration<double, std::milli>(t2 - t1).count());
+  }
+  return s;
 }
 
 rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
