@@ -19,7 +19,10 @@
 // buffers through CUDA IPC and allocate with plain cudaMalloc (rei_api.cu).
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <vector>
@@ -74,7 +77,13 @@ cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
   const size_t want = round_up(bytes ? bytes : 1);
   std::lock_guard<std::mutex> lk(g_mu);
   if ((*p = take_cached(dev, want)) != nullptr) return cudaSuccess;
+  static const bool trace = getenv("REI_TRACE") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   e = cudaMalloc(p, want);
+  if (trace)
+    fprintf(stderr, "[rei_devmem] cudaMalloc %zu bytes: %.3f ms (%s)\n", want,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+            cudaGetErrorString(e));
   if (e == cudaErrorMemoryAllocation) {
     cudaGetLastError();  // not sticky: clear it, return the idle blocks and retry once
     release_device(dev);

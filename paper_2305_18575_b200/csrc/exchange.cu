@@ -51,13 +51,36 @@ __global__ void k_select(const uint32_t* __restrict__ cs, const unsigned long lo
   }
 }
 
+// Sort key of a one-word CS: its bitmap position (levels.cu bm_pos: the n-bit CS
+// bit-reversed).
+__global__ void k_level_keys(const uint32_t* __restrict__ cs, uint64_t m, uint32_t n, uint32_t* __restrict__ keys,
+                             uint32_t* __restrict__ pos) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    keys[i] = n ? __brev(cs[i]) >> (32 - n) : 0u;
+    pos[i] = (uint32_t)i;
+  }
+}
+
+__global__ void k_gather_level(const uint32_t* __restrict__ cs, const unsigned long long* __restrict__ bp,
+                               const uint32_t* __restrict__ perm, uint64_t m, uint32_t* __restrict__ out_cs,
+                               unsigned long long* __restrict__ out_bp) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t j = perm[i];
+    out_cs[i] = cs[j];
+    out_bp[i] = bp[j];
+  }
+}
+
+// Scratch buffers grow geometrically and come from the caching allocator (devmem.cu).
 template <typename T>
 bool ensure(void** p, size_t* cap, size_t bytes, cudaStream_t st) {
   if (*cap >= bytes) return true;
-  if (*p) cudaFreeAsync(*p, st);
+  const size_t want = std::max(bytes, 2 * *cap);
+  dev_free(*p, st);
   *p = nullptr;
-  if (cudaMallocAsync(p, bytes, st) != cudaSuccess) return false;
-  *cap = bytes;
+  *cap = 0;
+  if (dev_alloc(p, want, st) != cudaSuccess) return false;
+  *cap = want;
   return true;
 }
 
@@ -113,9 +136,49 @@ bool merge_level(int W32, const uint32_t* g_cs, const unsigned long long* g_bp, 
   return cudaGetLastError() == cudaSuccess;
 }
 
+// Reorder a finished one-word level by bitmap position (a stable radix sort of the
+// level's entries with their back-pointers).  Consecutive cached operands then differ
+// mostly in their short-word bits, so the 32 candidates of a warp group (one uniform
+// operand x 32 consecutive operands) probe few distinct bitmap sectors.  The order of a
+// level is free: it is fixed before the level is used as an operand, back-pointers
+// refer to operand indices in that order, and every rank sorts identically.
+bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, MergeScratch& s, cudaStream_t st,
+                std::string& err, uint64_t* launches) {
+  if (m < 2) return true;
+  if (m >= 0xffffffffull) { err = "level too large to sort"; return false; }
+  const int grid = (int)std::min<uint64_t>((m + 255) / 256, 148 * 8);
+  bool ok = ensure<unsigned long long>(&s.keys, &s.keys_cap, m * 8, st) &&
+            ensure<unsigned long long>(&s.keys2, &s.keys2_cap, m * 8, st) &&
+            ensure<uint32_t>(&s.pos, &s.pos_cap, m * 4, st) && ensure<uint32_t>(&s.pos2, &s.pos2_cap, m * 4, st);
+  if (!ok) { err = "level sort scratch allocation failed"; return false; }
+  auto* keys = static_cast<uint32_t*>(s.keys);
+  auto* keys2 = static_cast<uint32_t*>(s.keys2);
+  auto* pos = static_cast<uint32_t*>(s.pos);
+  auto* pos2 = static_cast<uint32_t*>(s.pos2);
+  k_level_keys<<<grid, 256, 0, st>>>(cs, m, n, keys, pos);
+  size_t t1 = 0;
+  const int end_bit = (int)std::max<uint32_t>(1, n);
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, pos, pos2, (int)m, 0, end_bit, st);
+  if (!ensure<uint8_t>(&s.temp, &s.temp_cap, t1, st)) { err = "cub temp"; return false; }
+  if (cub::DeviceRadixSort::SortPairs(s.temp, t1, keys, keys2, pos, pos2, (int)m, 0, end_bit, st) != cudaSuccess) {
+    err = "level sort failed";
+    return false;
+  }
+  // gather into the (now free) key buffers, then copy back in place
+  auto* tmp_bp = static_cast<unsigned long long*>(s.keys);
+  auto* tmp_cs = static_cast<uint32_t*>(s.keys2);
+  k_gather_level<<<grid, 256, 0, st>>>(cs, bp, pos2, m, tmp_cs, tmp_bp);
+  if (cudaMemcpyAsync(cs, tmp_cs, m * 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess ||
+      cudaMemcpyAsync(bp, tmp_bp, m * 8, cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+    err = "level sort copy failed";
+    return false;
+  }
+  *launches += 3;
+  return cudaGetLastError() == cudaSuccess;
+}
+
 void free_merge_scratch(MergeScratch& s) {
-  cudaFree(s.keys); cudaFree(s.keys2); cudaFree(s.pos); cudaFree(s.pos2); cudaFree(s.flags);
-  cudaFree(s.scan); cudaFree(s.temp);
+  for (void* p : {s.keys, s.keys2, s.pos, s.pos2, s.flags, s.scan, s.temp}) dev_free(p, nullptr);
   s = MergeScratch{};
 }
 

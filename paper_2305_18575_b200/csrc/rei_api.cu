@@ -174,6 +174,7 @@ struct Ctx {
   std::vector<uint64_t> sh_used, sh_slabs;  // every owner's arena / slab fill
 
   int concurrency = 0;
+  bool sort_levels = false;  // bitmap mode: reorder each finished level by bitmap position
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
@@ -1059,6 +1060,14 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
       c->result.candidates = cand;
       c->result.last_complete_cost = (uint32_t)cost;
       if (otf_now) continue;  // nothing cached at this level
+      if (c->sort_levels && lv.size >= (1u << 14)) {  // bitmap mode: order by bitmap position (exchange.cu)
+        std::string err;
+        if (!sort_level((uint32_t)c->tab.n, c->arena + lv.begin, c->bp + lv.begin, lv.size, c->merge, c->stream,
+                        err, &c->launches)) {
+          c->err = err;
+          return REI_ECUDA;
+        }
+      }
       // transposed copy of level c (the sliced-operand layout for later levels)
       if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
         if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
@@ -1762,6 +1771,10 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   c->d2h_bytes += 64 + 8ull * c->tab.n;  // table summary + IC keys
   c->W32 = next_pow2_words(c->tab.n);
   c->mode = (c->tab.n <= 32) ? DEDUP_BITMAP : (c->W32 == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
+  // (A/B on B200: sorting the finished levels cuts the concat kernel's time 5-8 %, but
+  // the sorts cost as much on Table 1 row 8 and move row 1's answer later in level 28
+  // -- opt-in only)
+  c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_LEVEL_SORT") != nullptr;
   if (!c->budget) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);

@@ -47,11 +47,14 @@ bool merge_level(int W32, const uint32_t* g_cs, const unsigned long long* g_bp, 
                  unsigned long long* out_bp, uint64_t* out_count, MergeScratch& s, cudaStream_t st,
                  std::string& err, uint64_t* launches);
 void free_merge_scratch(MergeScratch& s);
+// Reorder a finished one-word (bitmap-mode) level by bitmap position, in place.
+bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, MergeScratch& s, cudaStream_t st,
+                std::string& err, uint64_t* launches);
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                uint64_t count, cudaStream_t st);
 
-// Process-wide caching allocators (devmem.cu): pooled stream-ordered device memory,
-// cached pinned host blocks.
+// Process-wide caching allocators (devmem.cu): size-keyed free lists of device blocks
+// and of pinned host blocks.
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
 uint64_t dev_pool_idle_bytes(int dev);

@@ -25,7 +25,7 @@ sys.path.insert(0, %r)
 import bench
 from paper_2305_18575_b200 import Solver
 spec, mc, _ = bench.WORKLOADS[%r]
-s = Solver.from_spec(spec, device=0)
+s = Solver.from_spec(spec, device=0, complete_final_level=%r)
 s.solve(mc)
 out = []
 for _ in range(%d):
@@ -49,17 +49,24 @@ def main():
     for f in sorted(glob.glob(os.path.join(PKG, "librei_b200_*.so"))):
         libs[os.path.basename(f)[len("librei_b200_"):-3]] = f
     modes = [m for m in os.environ.get("AB_CONC", "").split(",") if m]  # REI_CONCURRENT modes
+    # AB_ENVS="tag:K=V,K2=V2;tag2:K=V": extra environment variants of every library
+    envs = [("", {})]
+    for item in [x for x in os.environ.get("AB_ENVS", "").split(";") if x]:
+        tag, kvs = item.split(":", 1)
+        envs.append((tag, dict(kv.split("=", 1) for kv in kvs.split(","))))
     runs_of = {}
     for name, path in libs.items():
         for m in modes or [None]:
-            runs_of[name if m is None else f"{name}/c{m}"] = (path, m)
+            for tag, extra in envs:
+                key = (name if m is None else f"{name}/c{m}") + (f"/{tag}" if tag else "")
+                runs_of[key] = (path, m, extra)
     res = {k: [] for k in runs_of}
     for rnd in range(2):
-        for name, (path, m) in runs_of.items():
-            env = dict(os.environ, REI_LIB=path)
+        for name, (path, m, extra) in runs_of.items():
+            env = dict(os.environ, REI_LIB=path, **extra)
             if m is not None:
                 env["REI_CONCURRENT"] = m
-            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, workload, reps)], env=env,
+            out = subprocess.run([sys.executable, "-c", CHILD % (ROOT, workload, os.environ.get("AB_COMPLETE") == "1", reps)], env=env,
                                  capture_output=True, text=True, timeout=600)
             if out.returncode != 0:
                 print(name, "FAILED", out.stderr[-400:])
