@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "rei_common.cuh"
@@ -158,9 +159,14 @@ bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, Me
   k_level_keys<<<grid, 256, 0, st>>>(cs, m, n, keys, pos);
   size_t t1 = 0;
   const int end_bit = (int)std::max<uint32_t>(1, n);
-  cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, pos, pos2, (int)m, 0, end_bit, st);
+  // order by the top 12 key bits only (they select the bitmap sector; one radix pass
+  // fewer than the full key); REI_LEVEL_SORT_BITS=b overrides
+  const char* sb = getenv("REI_LEVEL_SORT_BITS");
+  const int begin_bit = std::max(0, end_bit - (sb ? atoi(sb) : 12));
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, pos, pos2, (int)m, begin_bit, end_bit, st);
   if (!ensure<uint8_t>(&s.temp, &s.temp_cap, t1, st)) { err = "cub temp"; return false; }
-  if (cub::DeviceRadixSort::SortPairs(s.temp, t1, keys, keys2, pos, pos2, (int)m, 0, end_bit, st) != cudaSuccess) {
+  if (cub::DeviceRadixSort::SortPairs(s.temp, t1, keys, keys2, pos, pos2, (int)m, begin_bit, end_bit, st) !=
+      cudaSuccess) {
     err = "level sort failed";
     return false;
   }

@@ -414,6 +414,12 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
         word[g] = need ? p.dedup.bitmap[pos[g] >> 5] : kFull;
 #endif
       }
+      // deep levels: > 99.9 % of the probes hit; one warp vote skips the insert /
+      // append code (and its per-candidate branches) for a batch with no miss at all
+      bool anymiss = false;
+#pragma unroll
+      for (int g = 0; g < G; ++g) anymiss |= !(word[g] & (1u << (pos[g] & 31)));
+      if (!__any_sync(__activemask(), anymiss)) return;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const uint32_t bit = 1u << (pos[g] & 31);

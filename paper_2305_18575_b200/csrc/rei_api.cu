@@ -1771,10 +1771,10 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   c->d2h_bytes += 64 + 8ull * c->tab.n;  // table summary + IC keys
   c->W32 = next_pow2_words(c->tab.n);
   c->mode = (c->tab.n <= 32) ? DEDUP_BITMAP : (c->W32 == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
-  // (A/B on B200: sorting the finished levels cuts the concat kernel's time 5-8 %, but
-  // the sorts cost as much on Table 1 row 8 and move row 1's answer later in level 28
-  // -- opt-in only)
-  c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_LEVEL_SORT") != nullptr;
+  // Finished levels are reordered by the top 12 bits of their bitmap position (A/B on
+  // B200, full final level: Table 1 row 1 67.5 -> 63.6 ms, row 8 neutral; a full 25-bit
+  // sort cut the kernels as much but cost more).  REI_NO_LEVEL_SORT disables it.
+  c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_NO_LEVEL_SORT") == nullptr;
   if (!c->budget) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);

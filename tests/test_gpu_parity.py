@@ -294,3 +294,24 @@ def test_onthefly_parity(cap, otf):
         assert precise(rg.regex, sp.P, sp.N)
     for c in range(1, min(first_otf, ro.last_complete_cost + 1)):
         assert sorted(g.level_cs(c)) == sorted(o.level_cs(c)), c
+
+
+@pytest.mark.parametrize("bits", [None, "25"])
+def test_level_sort_mode_parity(monkeypatch, bits):
+    # finished bitmap-mode levels (>= 2^14 entries) are reordered by bitmap position
+    # (default: top 12 bits; "25": the whole key); level sets, counts and every
+    # back-pointer must be unaffected
+    if bits:
+        monkeypatch.setenv("REI_LEVEL_SORT_BITS", bits)
+    sp = specgen.TABLE1_ROW1
+    o, g, ro, rg = compare_search(sp, 16)
+    assert max(l.unique for l in rg.levels) >= 1 << 14  # some level was sorted
+    ic = g.ic()
+    idx = {w: i for i, w in enumerate(ic)}
+    rnd = random.Random(7)
+    for c in (14, 15, 16):  # entries built from sorted operand levels
+        cs_list = g.level_cs(c)
+        for i in rnd.sample(range(len(cs_list)), 60):
+            rx = g.entry_regex(c, i)
+            assert sum(1 << idx[w] for w in language_on(rx, ic)) == cs_list[i], (c, i, rx)
+            assert re_cost(parse(rx), sp.costs) == c
