@@ -172,26 +172,38 @@ bool run_precompute(const std::vector<std::vector<uint8_t>>& P, const std::vecto
   void* d_tmp = nullptr;
   TableOut* d_out = nullptr;
   size_t tmp_sort = 0, tmp_uniq = 0;
-  CK(cudaMallocAsync(&d_syms, syms.size(), st));
-  CK(cudaMallocAsync(&d_off, nstr * 4, st));
-  CK(cudaMallocAsync(&d_len, nstr * 4, st));
-  CK(cudaMallocAsync(&d_koff, nstr * 8, st));
-  CK(cudaMallocAsync(&d_keys, total * 8, st));
-  CK(cudaMallocAsync(&d_sorted, total * 8, st));
-  CK(cudaMallocAsync(&d_n, sizeof(int), st));
-  CK(cudaMallocAsync(&d_out, sizeof(TableOut), st));
+  // CUB temp sizes first (size queries do not touch the buffers), then ONE scratch
+  // block from the caching allocator (devmem.cu) carved into the precompute buffers
+  cub::DeviceRadixSort::SortKeys(nullptr, tmp_sort, d_keys, d_sorted, (int)total, 0, 64, st);
+  cub::DeviceSelect::Unique(nullptr, tmp_uniq, d_sorted, d_keys, d_n, (int)total, st);
+  const size_t sizes[10] = {syms.size(), nstr * 4, nstr * 4, nstr * 8, total * 8, total * 8, sizeof(int),
+                            sizeof(TableOut), nstr * 8, std::max(tmp_sort, tmp_uniq)};
+  size_t offs[10], scratch_bytes = 0;
+  for (int i = 0; i < 10; ++i) {
+    offs[i] = scratch_bytes;
+    scratch_bytes += (sizes[i] + 255) / 256 * 256;
+  }
+  void* scratch = nullptr;
+  CK(dev_alloc(&scratch, scratch_bytes, st));
+  auto at = [&](int i) { return static_cast<void*>(static_cast<char*>(scratch) + offs[i]); };
+  d_syms = static_cast<uint8_t*>(at(0));
+  d_off = static_cast<uint32_t*>(at(1));
+  d_len = static_cast<uint32_t*>(at(2));
+  d_koff = static_cast<uint64_t*>(at(3));
+  d_keys = static_cast<unsigned long long*>(at(4));
+  d_sorted = static_cast<unsigned long long*>(at(5));
+  d_n = static_cast<int*>(at(6));
+  d_out = static_cast<TableOut*>(at(7));
+  d_ex = static_cast<unsigned long long*>(at(8));
+  d_tmp = at(9);
   CK(cudaMemcpyAsync(d_syms, syms.data(), syms.size(), cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_off, off.data(), nstr * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_len, len.data(), nstr * 4, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d_koff, koff.data(), nstr * 8, cudaMemcpyHostToDevice, st));
 
-  CK(cudaMallocAsync(&d_ex, nstr * 8, st));
   k_enum_keys<<<nstr, maxlen + 1, 0, st>>>(d_syms, d_off, d_len, d_koff, k, d_keys, d_ex);
   CK(cudaGetLastError());
   ++*launches;
-  cub::DeviceRadixSort::SortKeys(nullptr, tmp_sort, d_keys, d_sorted, (int)total, 0, 64, st);
-  cub::DeviceSelect::Unique(nullptr, tmp_uniq, d_sorted, d_keys, d_n, (int)total, st);
-  CK(cudaMallocAsync(&d_tmp, std::max(tmp_sort, tmp_uniq), st));
   CK(cub::DeviceRadixSort::SortKeys(d_tmp, tmp_sort, d_keys, d_sorted, (int)total, 0, 64, st));
   CK(cub::DeviceSelect::Unique(d_tmp, tmp_uniq, d_sorted, d_keys, d_n, (int)total, st));
   *launches += 4;  // CUB passes (approximate: histogram/onesweep/select)
@@ -214,16 +226,7 @@ bool run_precompute(const std::vector<std::vector<uint8_t>>& P, const std::vecto
   if (h.n > 0)
     CK(cudaMemcpyAsync(t.ic_keys.data(), d_keys, (size_t)h.n * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  cudaFreeAsync(d_syms, st);
-  cudaFreeAsync(d_off, st);
-  cudaFreeAsync(d_len, st);
-  cudaFreeAsync(d_koff, st);
-  cudaFreeAsync(d_keys, st);
-  cudaFreeAsync(d_sorted, st);
-  cudaFreeAsync(d_ex, st);
-  cudaFreeAsync(d_n, st);
-  cudaFreeAsync(d_tmp, st);
-  cudaFreeAsync(d_out, st);
+  dev_free(scratch, st);
   return err.empty();
 }
 
