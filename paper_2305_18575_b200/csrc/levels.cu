@@ -799,6 +799,12 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
   }
   // split masks: bit of the uniform operand that enables split k of word q*32+lane
   uint32_t mlo[W][MAXK], mhi[W][MAXK];
+#ifndef REI_FOLD_SEL
+  uint32_t shk[MAXK];
+  // bit `lane` of x as 0/1 = umulhi(x & 2^lane, 2^(32-lane)); lane 0 (word eps) needs no
+  // x[w] ? T[eps] term: it equals the x[eps] ? T[w] term there
+  const uint32_t shw = lane ? (1u << (32 - lane)) : 0u;
+#endif
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     const uint32_t w = q * 32 + lane;
@@ -810,6 +816,10 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
       const uint32_t fixed = SLICE_A ? (sp & 0xffffu) : (sp >> 16);
       mlo[q][k] = (ok && fixed < 32) ? (1u << fixed) : 0u;
       mhi[q][k] = (ok && fixed >= 32) ? (1u << (fixed & 31)) : 0u;
+#ifndef REI_FOLD_SEL
+      // 2^(32-u): umulhi(x & 2^u, 2^(32-u)) = bit u of x as 0/1 (u >= 1: a proper prefix)
+      if (q == 0) shk[k] = (ok && fixed >= 1 && fixed < 32) ? (1u << (32 - fixed)) : 0u;
+#endif
     }
   }
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
@@ -890,6 +900,34 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
           uint32_t x[W];
 #pragma unroll
           for (int q = 0; q < W; ++q) x[q] = __shfl_sync(kFull, xs[q], ui & 31);
+#ifndef REI_FOLD_SEL
+          if constexpr (W == 1) {
+            // one-word CSs: the fold's selects as 0/1 multiplies on the otherwise idle
+            // FMA pipe (b = a bit of x as 0/1 via umulhi, term = t * b), merged with
+            // 3-input ORs on the ALU pipe (A/B on B200: -2.4..3.5 % solve time; the
+            // concat kernel is ALU-bound once the probes hit L1)
+            auto mul = [](uint32_t t, uint32_t b) {
+              uint32_t r;
+              asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(t), "r"(b));
+              return r;
+            };
+            const uint32_t be = x[0] & 1u, bw = __umulhi(x[0] & lanebit, shw);
+            uint32_t bk[MAXK];
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k) bk[k] = __umulhi(x[0] & mlo[0][k], shk[k]);
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+              const int g = gx * SB + j;
+              uint32_t acc = mul(T[j][0], be) | mul(Teps[j], bw);
+#pragma unroll
+              for (int k = 0; k < MAXK; ++k) acc |= mul(tk[j][0][k], bk[k]);
+              cs[g][0] = acc;
+              valid[g] = FULL ? lane_ok[j] : (lane_ok[j] && ui < nu_item);
+            }
+            xk[gx][0] = x[0];
+            continue;
+          }
+#endif
           // enable masks of this operand (all-ones / zero), shared by the SB slabs:
           // epsilon splits (x[eps] -> T[w], x[w] -> T[eps]) and the proper splits
           const uint32_t me = (x[0] & 1u) ? kFull : 0u;
@@ -1022,8 +1060,21 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 
           for (int q = 0; q < W; ++q) y[j][q] = 0;
         }
       }
-      for (uint32_t ub = 0; ub < nu_item; ++ub) {
-        if (tri && u0 + ub >= s_last * 32 + 31) break;  // no j > i left in these slabs
+      // operand ub pairs with this lane's slab-j operand iff ub < dlim[j] (triangular
+      // blocks: j > i, i.e. (s + j) * 32 + lane > u0 + ub); 32-bit, set once per pass
+      int dlim[G];
+      uint32_t ub_end = nu_item;
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const long long d = (long long)((s + j) * 32 + lane) - (long long)u0;
+        dlim[j] = !lane_ok[j] ? 0 : (!tri ? 64 : (int)max(0LL, min(d, 64LL)));
+        evaluated += (uint32_t)min(dlim[j], (int)nu_item);
+      }
+      if (tri) {  // no j > i left in these slabs past ub_end
+        const long long e = (long long)(s_last * 32 + 31) - (long long)u0;
+        ub_end = (uint32_t)max(0LL, min(e, (long long)nu_item));
+      }
+      for (uint32_t ub = 0; ub < ub_end; ++ub) {
         uint32_t x[W];
         if (W <= 2) {
 #pragma unroll
@@ -1037,9 +1088,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 
         for (int j = 0; j < G; ++j) {
 #pragma unroll
           for (int q = 0; q < W; ++q) cs[j][q] = x[q] | y[j][q];
-          valid[j] = lane_ok[j] && (!tri || (s + j) * 32 + lane > u0 + ub);
+          valid[j] = (int)ub < dlim[j];
           skip[j] = cs_equal<W>(cs[j], x) || cs_equal<W>(cs[j], y[j]);
-          evaluated += valid[j] ? 1u : 0u;
         }
         process_batch<W, G, SH>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u0 + ub;
