@@ -376,10 +376,21 @@ __device__ __forceinline__ void on_new(const LevelParams& p, const uint32_t (&cs
 
 // stage != nullptr: called by the whole warp in converged code; new CSs go through the
 // warp's shared-memory stage.  stage == nullptr: per-lane warp-aggregated append.
-template <int W, int G, bool SH = false, class RankF>
+// REVCS (one-word CSs from the concat fast path): cs holds the CS bit-reversed in 32
+// bits (its bitmap position is then cs >> (32 - n)); the rare paths reverse it back.
+template <int W, int G, bool SH = false, bool REVCS = false, class RankF>
 __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&cs)[G][W], const bool (&valid)[G],
                                               const bool (&skip)[G], RankF rank_of,
                                               WarpStage<W>* stage = nullptr) {
+  static_assert(!REVCS || W == 1, "reversed CSs are one-word only");
+  if (REVCS) {
+    if (p.otf) {  // (rare mode) back to the plain layout, then the common code
+#pragma unroll
+      for (int g = 0; g < G; ++g) cs[g][0] = __brev(cs[g][0]);
+      process_batch<W, G, SH, false>(p, cs, valid, skip, rank_of, stage);
+      return;
+    }
+  }
   if (p.otf) {  // OnTheFly: the cache is full -- check only (a cached operand is never precise)
 #pragma unroll
     for (int g = 0; g < G; ++g)
@@ -407,7 +418,7 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         const bool need = valid[g] && !skip[g];
-        pos[g] = bm_pos(cs[g][0], p.n);
+        pos[g] = REVCS ? cs[g][0] >> (32 - p.n) : bm_pos(cs[g][0], p.n);
 #ifdef REI_PROBE_CG  // (A/B) probe through L2 only
         word[g] = need ? __ldcg(&p.dedup.bitmap[pos[g] >> 5]) : kFull;
 #else
@@ -427,6 +438,7 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
         if (!(word[g] & bit)) {
           const uint32_t old = atomicOr(&p.dedup.bitmap[pos[g] >> 5], bit);
           isnew[g] = !(old & bit);
+          if (REVCS) cs[g][0] = __brev(cs[g][0]);  // plain layout for the test / append
           if (!stage && isnew[g]) on_new<W>(p, cs[g], rank_of, g);  // rare: direct append
         }
       }
@@ -772,14 +784,24 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
   uint32_t* s_src = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);  // [MAXK][NW]
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  // REVL (one-word CSs): lane l computes the slice of word 31 - l, so the transposed
+  // candidate comes out bit-reversed -- its bitmap position is one shift away
+#ifdef REI_NO_REVLANES
+  constexpr bool REVL = false;
+#else
+  constexpr bool REVL = (W == 1);
+#endif
+  auto word_of = [](uint32_t l) { return REVL ? 31u - l : l; };  // word <-> lane (W = 1)
   for (int i = threadIdx.x; i < MAXK * NW; i += blockDim.x) {
-    const uint32_t sp = p.split[(size_t)(i / NW) * kMaxNW + (i % NW)];
-    s_src[i] = SLICE_A ? (sp >> 16) : (sp & 0xffffu);  // word of the sliced slab
+    const uint32_t sp = p.split[(size_t)(i / NW) * kMaxNW + word_of(i % NW)];
+    const uint32_t v = SLICE_A ? (sp >> 16) : (sp & 0xffffu);  // word of the sliced slab
+    s_src[i] = REVL ? word_of(v) : v;                            // ... = the lane holding it
   }
   __syncthreads();
 
   const uint32_t lane = lane_id();
-  const uint32_t lanebit = 1u << lane;
+  const uint32_t wl = word_of(lane);  // this lane's word (W = 1; q * 32 + lane otherwise)
+  const uint32_t lanebit = 1u << wl;
 #ifdef REI_TRANSPOSE_BFLY  // (A/B) the butterfly with per-lane masks / rotations
   const TransposeLane tr(lane);
   auto pre = [](uint32_t v) { return v; };
@@ -803,11 +825,11 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
   uint32_t shk[MAXK];
   // bit `lane` of x as 0/1 = umulhi(x & 2^lane, 2^(32-lane)); lane 0 (word eps) needs no
   // x[w] ? T[eps] term: it equals the x[eps] ? T[w] term there
-  const uint32_t shw = lane ? (1u << (32 - lane)) : 0u;
+  const uint32_t shw = wl ? (1u << (32 - wl)) : 0u;
 #endif
 #pragma unroll
   for (int q = 0; q < W; ++q) {
-    const uint32_t w = q * 32 + lane;
+    const uint32_t w = q * 32 + wl;
     const uint32_t ns = p.nsplit[w];
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) {
@@ -857,8 +879,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
         const bool slab_ok = s + j < s1;  // warp-uniform
         lane_ok[j] = slab_ok && (s + j) * 32 + lane < ns;
 #pragma unroll
-        for (int q = 0; q < W; ++q) T[j][q] = slab_ok ? p.tarena[(slab_base + s + j) * NW + q * 32 + lane] : 0u;
-        Teps[j] = __shfl_sync(kFull, T[j][0], 0);
+        for (int q = 0; q < W; ++q) T[j][q] = slab_ok ? p.tarena[(slab_base + s + j) * NW + q * 32 + wl] : 0u;
+        Teps[j] = __shfl_sync(kFull, T[j][0], word_of(0));
 #pragma unroll
         for (int q = 0; q < W; ++q) {
 #pragma unroll
@@ -968,8 +990,13 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
         }
         // equals its uniform operand: cached (an x.y == y filter measured slower: DESIGN.md)
 #pragma unroll
-        for (int g = 0; g < G; ++g) skip[g] = cs_equal<W>(cs[g], xk[g / SB]);
-        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+        for (int g = 0; g < G; ++g) {
+          uint32_t xc[W];
+#pragma unroll
+          for (int q = 0; q < W; ++q) xc[q] = REVL ? __brev(xk[g / SB][q]) : xk[g / SB][q];
+          skip[g] = cs_equal<W>(cs[g], xc);
+        }
+        process_batch<W, G, false, REVL>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u0 + ub + g / SB;
           const unsigned long long sj = (s + g % SB) * 32 + lane;
           return cand_off + (SLICE_A ? sj * nb + ui : ui * nb + sj);
