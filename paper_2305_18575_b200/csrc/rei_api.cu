@@ -1707,25 +1707,6 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   }
   auto fail = [&](const std::string& m) { g_init_error = m; return REI_ECUDA; };
   phase("validate + stream");
-  {
-    const char* ev = getenv("REI_CONCURRENT");
-    c->concurrency = ev ? std::max(0, std::min(4, atoi(ev))) : 3;
-    // 3: concat on a high-priority stream, union on a low-priority one; 4: the reverse
-    // (union candidates are the cheaper ones: with an early exit, cheapest first)
-    const int nstreams = std::min(3, c->concurrency);
-    if (nstreams >= 1) {
-      int prio_lo = 0, prio_hi = 0;
-      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-      const int low = c->concurrency == 3 ? 1 : c->concurrency == 4 ? 2 : -1;
-      for (int i = 0; i < nstreams; ++i)
-        if (cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking, i == low ? prio_lo : prio_hi) !=
-                cudaSuccess ||
-            cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
-          return fail("auxiliary stream creation failed");
-      if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
-        return fail("event creation failed");
-    }
-  }
   if (c->dmalloc(&c->tab.split, sizeof(uint32_t) * kMaxSplitRows * kMaxNW) != cudaSuccess ||
       c->dmalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
       c->dmalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
@@ -1775,6 +1756,32 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   // B200, full final level: Table 1 row 1 67.5 -> 63.6 ms, row 8 neutral; a full 25-bit
   // sort cut the kernels as much but cost more).  REI_NO_LEVEL_SORT disables it.
   c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_NO_LEVEL_SORT") == nullptr;
+  {
+    // A level's kernels run concurrently on auxiliary streams (REI_CONCURRENT):
+    // 0 = one stream; 1 = ? / * on their own stream; 2 = also union on its own stream
+    // (auxiliary streams at high priority, concat on the context's stream); 3 = concat on
+    // a high-priority stream, union on a low-priority one; 4 = 3 with the priorities
+    // swapped.  Default (A/B on B200): 2 for the bitmap dedup (L2-resident, ALU-bound
+    // kernels: Table 1 row 1 37.7 -> 30.9 ms, row 8 -4 %, full levels within 2 %), 3 for
+    // the HBM hash sets (two-word C2: 253 -> 212 ms -- the DRAM-bound kernels interfere
+    // less when concat has priority).
+    const char* ev = getenv("REI_CONCURRENT");
+    c->concurrency = ev ? std::max(0, std::min(4, atoi(ev))) : (c->mode == DEDUP_BITMAP ? 2 : 3);
+    const int nstreams = std::min(3, c->concurrency);
+    if (nstreams >= 1) {
+      int prio_lo = 0, prio_hi = 0;
+      cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+      const int low = c->concurrency == 3 ? 1 : c->concurrency == 4 ? 2 : -1;
+      for (int i = 0; i < nstreams; ++i)
+        if (cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking, i == low ? prio_lo : prio_hi) !=
+                cudaSuccess ||
+            cudaEventCreateWithFlags(&c->ev_join[i], cudaEventDisableTiming) != cudaSuccess)
+          return fail("auxiliary stream creation failed");
+      if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
+        return fail("event creation failed");
+    }
+  }
+
   if (!c->budget) {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
