@@ -315,3 +315,26 @@ def test_level_sort_mode_parity(monkeypatch, bits):
             rx = g.entry_regex(c, i)
             assert sum(1 << idx[w] for w in language_on(rx, ic)) == cs_list[i], (c, i, rx)
             assert re_cost(parse(rx), sp.costs) == c
+
+
+def test_cached_allocator_reuse_and_release():
+    # contexts created after others were destroyed reuse their cached device / pinned
+    # blocks (devmem.cu); results must not depend on the blocks' previous contents, and
+    # rei_release_cached_memory may run at any time
+    from paper_2305_18575_b200 import release_cached_memory
+    cases = [(specgen.C1_TOY, 12), (W2[0][0], 16), (specgen.C1_TOY, 12), (W2[0][0], 16)]
+    want = {}
+    for i, (sp, K) in enumerate(cases):
+        g = gpu_solver(sp, complete_final_level=True)
+        r = g.solve(K)
+        key = sp.name or id(sp)
+        sets = [sorted(g.level_cs(c)) for c in range(1, r.cost + 1)]
+        if key in want:
+            assert (r.cost, sets) == want[key]
+        else:
+            ro = oracle.Oracle.from_spec(sp).solve(K, complete_final_level=True)
+            assert r.cost == ro.cost
+            want[key] = (r.cost, sets)
+        g.close()
+        if i == 1:
+            release_cached_memory()
