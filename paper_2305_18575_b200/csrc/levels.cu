@@ -775,7 +775,11 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 #endif
   constexpr int G = (W == 1) ? REI_CONCAT_G1 : 4;  // groups (probes per lane) in flight
   // slabs per pass: keep SB * W * MAXK shuffled slab words in registers (<= 16 + W * MAXK)
+#ifdef REI_SB1  // (A/B) slabs per pass for one-word CSs
+  constexpr int SB0 = (W == 1) ? REI_SB1 : ((W * MAXK <= 3) ? 4 : (W * MAXK <= 7 ? 2 : 1));
+#else
   constexpr int SB0 = (W * MAXK <= 3) ? 4 : (W * MAXK <= 7 ? 2 : 1);
+#endif
   constexpr int SB = SB0 < G ? SB0 : G;
   constexpr int GX = G / SB;  // uniform operands per batch
   static_assert(G % SB == 0 && 32 % GX == 0, "batch shape");
