@@ -20,6 +20,7 @@ CASES = [
     (specgen.gen_planted("01", "1(0+11)*0?", 8, 8, 6, 12, 0), 9, {}),   # indexed hash, W32=4
     (specgen.Spec("01", ("0" * 20, "1"), ("0" * 19, "11")), 10, {}),    # generic kernels
     (specgen.TABLE1_ROW1, 30, {"error": (20, 100)}),                # allowed error
+    (specgen.TABLE1_ROW1, 15, {}),                                  # level sort (levels >= 2^14)
     (specgen.C1_TOY.with_costs((1, 3, 3, 1, 3)), 40, {"max_entries": 160}),  # OnTheFly
 ]
 
