@@ -789,7 +789,13 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   };
   // fork: the level's kernels are independent (they read lower levels and insert
   // through atomics), so ? / * (and union) may run on auxiliary streams
-  const int conc = std::min(3, c->concurrency);
+  // small levels run on one stream: their kernels are launch-latency bound and the
+  // fork / join events would cost more than the overlap gains
+  uint64_t level_cand = nq + ns;
+  for (const Block& b : cat) level_cand += b.cand_count;
+  for (const Block& b : uni) level_cand += b.cand_count;
+  const uint64_t small = getenv("REI_SMALL_LEVEL") ? strtoull(getenv("REI_SMALL_LEVEL"), nullptr, 10) : 0;
+  const int conc = level_cand < small ? 0 : std::min(3, c->concurrency);
   cudaStream_t su = conc >= 1 ? c->aux[0] : c->stream;
   cudaStream_t sn = conc >= 2 ? c->aux[1] : c->stream;
   cudaStream_t sc = conc >= 3 ? c->aux[2] : c->stream;
