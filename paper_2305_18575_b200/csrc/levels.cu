@@ -992,13 +992,15 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
           for (int i = 0; i < G * W; ++i) v[i] = tr(v[i]);
 #endif
         }
-        // equals its uniform operand: cached (an x.y == y filter measured slower: DESIGN.md)
+        // equals its uniform operand: cached, no probe needed (two-word CSs, whose probes
+        // go to HBM; one-word probes hit L1, and the compare cost more than it saved:
+        // A/B -1 %; an x.y == y filter measured slower too: DESIGN.md)
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           uint32_t xc[W];
 #pragma unroll
           for (int q = 0; q < W; ++q) xc[q] = REVL ? __brev(xk[g / SB][q]) : xk[g / SB][q];
-          skip[g] = cs_equal<W>(cs[g], xc);
+          skip[g] = (W == 1) ? false : cs_equal<W>(cs[g], xc);
         }
         process_batch<W, G, false, REVL>(p, cs, valid, skip, [&](int g) {
           const unsigned long long ui = u0 + ub + g / SB;
