@@ -1284,6 +1284,22 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
         X[q] = p.tarena[(slab_s + s) * NW + q * 32 + lane];
         S[q] = (q == 0 && lane == 0) ? kFull : 0u;  // every star contains eps
       }
+      // X[u] does not change across the rounds: fetch the split prefixes once per slab
+      // (zero for absent splits), then each round shuffles only S[v]
+      uint32_t xu[W][MAXK];
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k) {
+          const uint32_t u = spl[q][k] >> 16;
+          uint32_t a = __shfl_sync(kFull, X[0], u & 31);
+          if (W == 2) {
+            const uint32_t a1 = __shfl_sync(kFull, X[W - 1], u & 31);
+            a = (u & 32) ? a1 : a;
+          }
+          xu[q][k] = spl[q][k] != 0xffffffffu ? a : 0u;
+        }
+      }
       for (uint32_t L = 1; L <= maxlen; ++L) {
         uint32_t add[W];
 #pragma unroll
@@ -1292,15 +1308,13 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
         for (int q = 0; q < W; ++q) {
 #pragma unroll
           for (int k = 0; k < MAXK; ++k) {
-            const uint32_t u = spl[q][k] >> 16, v = spl[q][k] & 0xffffu;
-            uint32_t xu = __shfl_sync(kFull, X[0], u & 31), sv = __shfl_sync(kFull, S[0], v & 31);
+            const uint32_t v = spl[q][k] & 0xffffu;
+            uint32_t sv = __shfl_sync(kFull, S[0], v & 31);
             if (W == 2) {
-              const uint32_t xu1 = __shfl_sync(kFull, X[W - 1], u & 31);
               const uint32_t sv1 = __shfl_sync(kFull, S[W - 1], v & 31);
-              xu = (u & 32) ? xu1 : xu;
               sv = (v & 32) ? sv1 : sv;
             }
-            if (spl[q][k] != 0xffffffffu) add[q] |= xu & sv;
+            add[q] |= xu[q][k] & sv;
           }
         }
 #pragma unroll
