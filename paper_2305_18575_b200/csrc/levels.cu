@@ -1308,6 +1308,9 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
         for (int q = 0; q < W; ++q) {
 #pragma unroll
           for (int k = 0; k < MAXK; ++k) {
+            // only the words of length L update in round L, and they have L - 1 proper
+            // splits: later split slots are skipped (warp-uniform)
+            if ((uint32_t)k + 1 >= L) break;
             const uint32_t v = spl[q][k] & 0xffffu;
             uint32_t sv = __shfl_sync(kFull, S[0], v & 31);
             if (W == 2) {
