@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -113,7 +114,8 @@ struct Ctx {
   rei_costs costs{};
   uint32_t err_num = 0, err_den = 1;
   uint32_t flags = 0;
-  uint64_t budget = 0;
+  uint64_t budget = 0;       // 0 until first needed (budget_of)
+  uint64_t budget_used = 0;  // bytes allocated before the budget was first queried
   uint64_t entry_limit = 0;  // rei_options.max_entries (0 = budget only)
   int otf_level = 0;         // first level checked in OnTheFly mode (0 = none)
 
@@ -596,9 +598,36 @@ rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
   return REI_OK;
 }
 
+// Device memory the context may use: rei_options.mem_budget_bytes, else 80 % of the
+// free HBM (plus the allocator's idle blocks), queried lazily: cudaMemGetInfo costs
+// 0.3-70 ms per call on B200 (measured), so a bitmap-mode context whose fixed-size
+// cache is small never asks.
+uint64_t budget_of(Ctx* c) {
+  if (!c->budget) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    if (!c->sharded) fr += dev_pool_idle_bytes(c->device);  // idle blocks the allocator keeps
+    c->budget = (uint64_t)(0.8 * (double)fr);
+    c->budget = c->budget > c->budget_used ? c->budget - c->budget_used : 0;
+  }
+  return c->budget;
+}
+
+// Total HBM of the current device, queried once per process and device.
+uint64_t device_total_bytes(int dev) {
+  static std::mutex mu;
+  static std::map<int, uint64_t> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  return cache[dev] = tot;
+}
+
 rei_status grow(Ctx* c, uint64_t need_entries) {
   if (c->sharded) return REI_OUT_OF_MEMORY;  // peers map the buffers: fixed at rei_init
-  uint64_t max_cap = c->budget / bytes_per_entry(c);
+  uint64_t max_cap = budget_of(c) / bytes_per_entry(c);
   if (c->entry_limit) max_cap = std::min<uint64_t>(max_cap, c->entry_limit);
   if (c->cap >= max_cap) return REI_OUT_OF_MEMORY;
   // x8 per growth: every growth rehashes the whole cache, so grow rarely
@@ -1788,29 +1817,29 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     }
   }
 
-  if (!c->budget) {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    if (!c->sharded) fr += dev_pool_idle_bytes(c->device);  // blocks the pool keeps for reuse
-    c->budget = (uint64_t)(0.8 * (double)fr);
-  }
   if (c->mode == DEDUP_BITMAP) {
     c->bitmap_words = std::max<uint64_t>(1, (1ull << c->tab.n) / 32);
     if (c->dmalloc(&c->bitmap, c->bitmap_words * 4) != cudaSuccess) return fail("bitmap allocation failed");
-    c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
+    if (c->budget) c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
+    else c->budget_used = c->bitmap_words * 4;  // charged when the budget is first queried
   }
   // bitmap mode: at most 2^n distinct CSs exist, so reserve them all up front (up to
-  // 2^28 entries); hash modes start at 2^20 entries and grow ahead of each level.
+  // 2^28 entries); hash modes start at 2^22 entries and grow ahead of each level.
   uint64_t cap0 = 1ull << 22;
   if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(1ull << 28, (1ull << c->tab.n) + 64);
-  cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, c->budget / bytes_per_entry(c.get())));
+  // the free-memory query is skipped when the initial cache is < 1/8 of the HBM
+  if (c->budget || c->sharded || cap0 * bytes_per_entry(c.get()) > device_total_bytes(c->device) / 8)
+    cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, budget_of(c.get()) / bytes_per_entry(c.get())));
+  phase("budget");
   if (c->sharded) {  // sized once: peers map these buffers, so they never move
-    cap0 = c->budget / bytes_per_entry(c.get());
+    cap0 = budget_of(c.get()) / bytes_per_entry(c.get());
     if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(cap0, (1ull << c->tab.n) + 64);
     if (c->entry_limit) cap0 = std::min<uint64_t>(cap0, c->entry_limit);
     cap0 = std::max<uint64_t>(cap0, 1024);
   }
+  phase("bitmap");
   if (alloc_arena(c.get(), cap0, 0, 0) != REI_OK) return fail(c->err);
+  phase("arena");
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) return fail("init sync failed");
   phase("dedup set + language cache");
   if (c->sharded && c->world > 1) {  // collective: map every rank's buffers (CUDA IPC)
