@@ -176,7 +176,8 @@ struct Ctx {
   std::vector<uint64_t> sh_used, sh_slabs;  // every owner's arena / slab fill
 
   int concurrency = 0;
-  bool sort_levels = false;  // bitmap mode: reorder each finished level by bitmap position
+  bool sort_levels = false;
+  bool union_first = false;  // bitmap mode: reorder each finished level by bitmap position
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
@@ -844,18 +845,22 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
       c->end_kernel(ep, n);
     }
   }
-  for (int r = 0; r < 2; ++r) {
-    if (catv[r].empty()) continue;
-    LevelParams pc = p;
-    pc.blocks = c->d_blocks + r * Ctx::kMaxBlocks;
-    pc.nblocks = (uint32_t)catv[r].size();
-    if (!share(items_of(catv[r]), pc)) continue;
-    EventPair ep;
-    c->begin_kernel(REI_K_CONCAT, ep, sc);
-    int n = launch_concat(c->W32, pc, r == 1, sc);
-    c->end_kernel(ep, n);
-  }
-  if (!uni.empty()) {
+  auto launch_cat = [&]() -> rei_status {
+    for (int r = 0; r < 2; ++r) {
+      if (catv[r].empty()) continue;
+      LevelParams pc = p;
+      pc.blocks = c->d_blocks + r * Ctx::kMaxBlocks;
+      pc.nblocks = (uint32_t)catv[r].size();
+      if (!share(items_of(catv[r]), pc)) continue;
+      EventPair ep;
+      c->begin_kernel(REI_K_CONCAT, ep, sc);
+      int n = launch_concat(c->W32, pc, r == 1, sc);
+      c->end_kernel(ep, n);
+    }
+    return REI_OK;
+  };
+  auto launch_uni = [&]() -> rei_status {
+    if (uni.empty()) return REI_OK;
     LevelParams pu = p;
     pu.blocks = c->d_blocks + 2 * Ctx::kMaxBlocks;
     pu.nblocks = (uint32_t)uni.size();
@@ -865,7 +870,11 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
       int n = launch_union(c->W32, pu, sn);
       c->end_kernel(ep, n);
     }
-  }
+    return REI_OK;
+  };
+  // REI_UNION_FIRST (A/B): the union kernel takes the SMs first (cheapest candidates
+  // first for an early exit)
+  if (c->union_first) { launch_uni(); launch_cat(); } else { launch_cat(); launch_uni(); }
   if (conc >= 1) {  // join
     for (int i = 0; i < conc; ++i) {
       CUDA_OK(c, cudaEventRecord(c->ev_join[i], c->aux[i]));
@@ -1791,6 +1800,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   // B200, full final level: Table 1 row 1 67.5 -> 63.6 ms, row 8 neutral; a full 25-bit
   // sort cut the kernels as much but cost more).  REI_NO_LEVEL_SORT disables it.
   c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_NO_LEVEL_SORT") == nullptr;
+  c->union_first = getenv("REI_UNION_FIRST") != nullptr;
   {
     // A level's kernels run concurrently on auxiliary streams (REI_CONCURRENT):
     // 0 = one stream; 1 = ? / * on their own stream; 2 = also union on its own stream
