@@ -20,6 +20,7 @@ has) on a bounded sample.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -248,6 +249,10 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     solver.reset_kernel_stats()
     launches0 = solver.launch_count()
+    # no Python garbage collection inside the timed regions (a full collection with torch
+    # loaded pauses the host for tens of ms, and the solve's host-side level loop with it)
+    gc.collect()
+    gc.disable()
     sampler = ClockSampler(local_rank)
     sampler.start()
     step_ms, cands, results = [], 0, []
@@ -381,6 +386,7 @@ def run_ours(args, rank, world, local_rank):
         e2e_cands += r2.candidates
         h2d += hb
         d2h += db
+    gc.enable()
     e2e = {"value": e2e_cands / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // n_e2e,
            "d2h_bytes_per_step": d2h // n_e2e,
            "time_to_minimal_re_ms": 1000 * e2e_s / n_e2e,
