@@ -282,18 +282,22 @@ def run_ours(args, rank, world, local_rank):
     # timed region a level's kernels overlap on concurrent streams (REI_CONCURRENT 2 or 3),
     # so one kernel's event span includes SMs lent to another; the per-kernel numbers
     # come from a sequential pass (REI_CONCURRENT=0, same workload, K steps, L2 flushed)
-    # -- the launch order ncu serialises too.
+    # -- the launch order ncu serialises too.  Concat goes first there (REI_UNION_FIRST=0):
+    # with union first on one stream, a union hit at c* makes the concat launches of that
+    # level exit at once, and their launch overhead would count against the kernel.
     kresults, kstep_ms, kernel_pass = results, step_ms, "timed region"
     if world == 1:
-        prev = os.environ.get("REI_CONCURRENT")
+        prev = {k: os.environ.get(k) for k in ("REI_CONCURRENT", "REI_UNION_FIRST")}
         os.environ["REI_CONCURRENT"] = "0"
+        os.environ["REI_UNION_FIRST"] = "0"
         try:
             ksolver = Solver.from_spec(spec, device=local_rank, stream=stream)
         finally:
-            if prev is None:
-                os.environ.pop("REI_CONCURRENT")
-            else:
-                os.environ["REI_CONCURRENT"] = prev
+            for k, v in prev.items():
+                if v is None:
+                    os.environ.pop(k)
+                else:
+                    os.environ[k] = v
         ksolver.solve(max_cost)
         torch.cuda.synchronize()
         ksolver.reset_kernel_stats()
@@ -311,7 +315,8 @@ def run_ours(args, rank, world, local_rank):
             kstep_ms.append(e0.elapsed_time(e1))
         kstats = ksolver.kernel_stats()
         ksolver.close()
-        kernel_pass = f"sequential-stream pass (REI_CONCURRENT=0), {args.steps} steps, L2 flushed"
+        kernel_pass = (f"sequential-stream pass (REI_CONCURRENT=0, REI_UNION_FIRST=0), {args.steps} steps, "
+                       "L2 flushed")
     dom = max(("concat", "union", "unary", "transpose"), key=lambda k: kstats[k][1])
     dom_launches, dom_ms = kstats[dom]
     evaluated = 0

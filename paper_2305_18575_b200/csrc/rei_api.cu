@@ -177,7 +177,7 @@ struct Ctx {
 
   int concurrency = 0;
   bool sort_levels = false;
-  bool union_first = false;  // bitmap mode: reorder each finished level by bitmap position
+  bool union_first = false;  // launch a level's union kernel before its concat kernels
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
@@ -872,8 +872,8 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     }
     return REI_OK;
   };
-  // REI_UNION_FIRST (A/B): the union kernel takes the SMs first (cheapest candidates
-  // first for an early exit)
+  // union first (bitmap dedup default, REI_UNION_FIRST): the union kernel takes the SMs
+  // first, so a precise union is met early at c* (see rei_init)
   if (c->union_first) { launch_uni(); launch_cat(); } else { launch_cat(); launch_uni(); }
   if (conc >= 1) {  // join
     for (int i = 0; i < conc; ++i) {
@@ -1800,7 +1800,16 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   // B200, full final level: Table 1 row 1 67.5 -> 63.6 ms, row 8 neutral; a full 25-bit
   // sort cut the kernels as much but cost more).  REI_NO_LEVEL_SORT disables it.
   c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_NO_LEVEL_SORT") == nullptr;
-  c->union_first = getenv("REI_UNION_FIRST") != nullptr;
+  // Launch order of a level's binary kernels (REI_UNION_FIRST=0/1 overrides).  With the
+  // bitmap dedup the union kernel goes first: the early exit at c* then no longer waits
+  // for the union CTAs to get SMs behind a full concat grid (A/B on B200, 15 interleaved
+  // solves each: Table 1 row 1 median 30.7 ms both, p90 37.5 -> 30.9 ms, max 118 ->
+  // 38 ms; row 8 equal).  The HBM hash sets keep concat first (C2 median 228 -> 296 ms
+  // with union first).
+  {
+    const char* uf = getenv("REI_UNION_FIRST");
+    c->union_first = uf ? atoi(uf) != 0 : c->mode == DEDUP_BITMAP;
+  }
   {
     // A level's kernels run concurrently on auxiliary streams (REI_CONCURRENT):
     // 0 = one stream; 1 = ? / * on their own stream; 2 = also union on its own stream
