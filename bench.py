@@ -275,6 +275,8 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
     launches = solver.launch_count() - launches0
     kstats = solver.kernel_stats()
+    ic_words = solver.ic()
+    solver.close()  # the kernel pass and the e2e solves below run one context at a time
     total_ms, all_cands = reduce_over_ranks(sum(step_ms), cands, dev, world, sum_work=not sharded)
     value = all_cands / (total_ms / 1000.0)
 
@@ -324,7 +326,7 @@ def run_ours(args, rank, world, local_rank):
         for l in rr.levels:
             evaluated += {"concat": l.eval_c, "union": l.eval_u}.get(dom, l.evaluated)
     w32 = results[0].cs_words
-    s_in = sum(max(0, len(w) - 1) for w in solver.ic())
+    s_in = sum(max(0, len(w) - 1) for w in ic_words)
     peaks, peaks_kind = load_peaks()
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
     alu_peak = 64 * 148 * sm_mhz * 1e6  # INT32 ALU-pipe lane-ops/s (B300_MICROARCH rt_SMSP=2)
