@@ -162,6 +162,24 @@ def test_generic_kernels_parity(sp, K, var, monkeypatch):
     compare_search(sp, K)
 
 
+@pytest.mark.parametrize("order", ["0", "1"])
+@pytest.mark.parametrize("conc", ["0", "2", "3"])
+@pytest.mark.parametrize("sp,K", RANDOM_W1[:2] + W2[:1], ids=ids(RANDOM_W1[:2] + W2[:1]))
+def test_launch_order_and_streams_parity(sp, K, order, conc, monkeypatch):
+    # a level's kernels are independent (REI_UNION_FIRST = launch order, REI_CONCURRENT =
+    # stream layout): every combination reaches the oracle's level sets, both in the
+    # complete-final-level mode and with the early exit
+    monkeypatch.setenv("REI_UNION_FIRST", order)
+    monkeypatch.setenv("REI_CONCURRENT", conc)
+    compare_search(sp, K)
+    o = oracle.Oracle.from_spec(sp)
+    ro = o.solve(K)
+    rg = gpu_solver(sp).solve(K)
+    assert (rg.status, rg.cost) == (ro.status, ro.cost)
+    if ro.status == "found" and rg.regex not in ("empty", "eps"):
+        assert precise(rg.regex, sp.P, sp.N)
+
+
 @pytest.mark.parametrize("sp", [specgen.Spec("01", ("0" * 20, "1"), ("0" * 19, "11")),
                                 specgen.Spec("01", ("0" * 40, "1"), ("0" * 39, "11"))],
                          ids=["w1-len20", "w2-len40"])
