@@ -1023,8 +1023,10 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 // ============================================================================
 // Union kernel: uniform operand x, lane t holds operand_t of the sliced level.
 template <int W, bool SH = false>
-#ifndef REI_UNION_MINB1
-#define REI_UNION_MINB1 3
+#ifndef REI_UNION_MINB1  // 4 CTAs/SM for one-word CSs (A/B on B200, scripts/ab_variants.py,
+                         // 14 interleaved solves: Table 1 row 1 30.4 -> 29.7 ms, row 8 equal;
+                         // 2 CTAs x 8 probes and 3 x 8 were slower)
+#define REI_UNION_MINB1 4
 #endif
 #ifndef REI_UNION_G1
 #define REI_UNION_G1 4
