@@ -51,11 +51,17 @@
 
 namespace {
 
-constexpr int kMaxWords = 8;  // |IC| <= 512 bits
-using CS = std::array<uint64_t, kMaxWords>;
+constexpr int kMaxWords = 8;  // |IC| <= 512 bits (the C ABI below always uses 8 words)
 
+// A CS is stored in W 64-bit words, W = the smallest of 1, 2, 4, 8 with 64 W >= |IC|
+// (power-of-two width, reading A16: the width is invisible to results;
+// it only sets the oracle's memory per cached CS).
+template <int W>
+using CSW = std::array<uint64_t, W>;
+
+template <int W>
 struct CSHash {
-  size_t operator()(const CS& c) const {
+  size_t operator()(const CSW<W>& c) const noexcept {
     size_t h = 1469598103934665603ull;
     for (uint64_t w : c) {
       h ^= std::hash<uint64_t>()(w) + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
@@ -64,23 +70,27 @@ struct CSHash {
   }
 };
 
-bool test_bit(const CS& c, int i) { return (c[i / 64] >> (i % 64)) & 1ull; }
-void set_bit(CS& c, int i) { c[i / 64] |= 1ull << (i % 64); }
-CS zero_cs() { CS c; c.fill(0); return c; }
+template <size_t W>
+bool test_bit(const std::array<uint64_t, W>& c, int i) { return (c[i / 64] >> (i % 64)) & 1ull; }
+template <size_t W>
+void set_bit(std::array<uint64_t, W>& c, int i) { c[i / 64] |= 1ull << (i % 64); }
+template <int W>
+CSW<W> zero_cs() { CSW<W> c; c.fill(0); return c; }
 
 enum Kind : int { K_SYM = 0, K_QUESTION = 1, K_STAR = 2, K_CONCAT = 3, K_UNION = 4,
                   K_EMPTY = 5, K_EPS = 6 };
 
 struct Prov {
-  int kind;   // Kind
-  int L;      // cost level of the left / only operand (or symbol index for K_SYM)
-  long i;     // index of the left / only operand in level L
-  int R;      // cost level of the right operand
-  long j;     // index of the right operand in level R
+  int32_t kind;  // Kind
+  int32_t L;     // cost level of the left / only operand (or symbol index for K_SYM)
+  uint32_t i;    // index of the left / only operand in level L
+  int32_t R;     // cost level of the right operand
+  uint32_t j;    // index of the right operand in level R
 };
 
+template <int W>
 struct Entry {
-  CS cs;
+  CSW<W> cs;
   Prov prov;
 };
 
@@ -91,7 +101,32 @@ struct LevelStat {
   int complete;
 };
 
-struct Oracle {
+// The ABI's view of one oracle instance (CSs cross it as 8 words).
+struct Search {
+  virtual ~Search() {}
+  virtual int n() const = 0;
+  virtual const std::string& ic_word(int k) const = 0;
+  virtual const std::vector<std::pair<int, int>>& gt_row(int w) const = 0;
+  virtual void masks8(uint64_t* pos8, uint64_t* neg8) const = 0;
+  virtual void op8(int op, const uint64_t* a, const uint64_t* b, uint64_t* out) const = 0;
+  virtual int run(int max_cost, long err_num, long err_den, bool complete_final_level,
+                  uint64_t max_entries, bool onthefly) = 0;
+  virtual int otf() const = 0;
+  virtual void result6(long long* out6, double* seconds) const = 0;
+  virtual const std::string& regex_text() const = 0;
+  virtual const std::vector<LevelStat>& level_stats() const = 0;
+  virtual long level_size(int cost) const = 0;
+  virtual long level_cs8(int cost, uint64_t* out, long cap) const = 0;
+  virtual std::string entry_regex(int cost, long i) const = 0;
+};
+
+template <int W>
+struct Oracle : Search {
+  using CS = CSW<W>;
+  using Entry = ::Entry<W>;
+  using CSHash = ::CSHash<W>;
+  static CS zero_cs() { return ::zero_cs<W>(); }
+
   std::string alphabet;
   std::vector<std::string> P, N;
   int c[5];  // (sym, ?, *, concat, union)
@@ -179,7 +214,7 @@ struct Oracle {
     for (auto& q : N) set_bit(neg_mask, index_of.at(q));
   }
 
-  int n() const { return (int)ic.size(); }
+  int n() const override { return (int)ic.size(); }
 
   // ---- IPS operations -------------------------------------
   CS one() const {  // 1(sigma) = [sigma = eps]
@@ -189,7 +224,7 @@ struct Oracle {
   }
   CS op_union(const CS& a, const CS& b) const {  // (r + s)(sigma) = r(sigma) v s(sigma)
     CS r;
-    for (int k = 0; k < kMaxWords; ++k) r[k] = a[k] | b[k];
+    for (int k = 0; k < W; ++k) r[k] = a[k] | b[k];
     return r;
   }
   // Algorithm 2, lines 5-14: fold over every split in gt[w].
@@ -217,7 +252,7 @@ struct Oracle {
   // examples is at most the allowed fraction of |P u N|.
   bool satisfies(const CS& cs) const {
     if (err_num == 0) {
-      for (int k = 0; k < kMaxWords; ++k) {
+      for (int k = 0; k < W; ++k) {
         if ((cs[k] & pos_mask[k]) != pos_mask[k]) return false;
         if ((cs[k] & neg_mask[k]) != 0) return false;
       }
@@ -385,7 +420,7 @@ struct Oracle {
         cand_level = 0;
         auto& A = levels[cost - c2];
         for (size_t i = 0; i < A.size() && !stop(); ++i)
-          emit(op_question(A[i].cs), Prov{K_QUESTION, cost - c2, (long)i, 0, 0});
+          emit(op_question(A[i].cs), Prov{K_QUESTION, cost - c2, (uint32_t)i, 0, 0});
         st.cand_q = cand_level;
       }
       // buildStar(c - cost(*))
@@ -393,7 +428,7 @@ struct Oracle {
         cand_level = 0;
         auto& A = levels[cost - c3];
         for (size_t i = 0; i < A.size() && !stop(); ++i)
-          emit(op_star(A[i].cs), Prov{K_STAR, cost - c3, (long)i, 0, 0});
+          emit(op_star(A[i].cs), Prov{K_STAR, cost - c3, (uint32_t)i, 0, 0});
         st.cand_s = cand_level;
       }
       // buildConcat(c - cost(.)) -- Algorithm 2: all (L, R) with L + R = c - c4,
@@ -406,7 +441,7 @@ struct Oracle {
         auto& B = levels[R];
         for (size_t i = 0; i < A.size() && !stop(); ++i)
           for (size_t j = 0; j < B.size() && !stop(); ++j)
-            emit(op_concat(A[i].cs, B[j].cs), Prov{K_CONCAT, L, (long)i, R, (long)j});
+            emit(op_concat(A[i].cs, B[j].cs), Prov{K_CONCAT, L, (uint32_t)i, R, (uint32_t)j});
       }
       st.cand_c = cand_level;
       // buildUnion(c - cost(+)) -- unordered pairs L <= R, i < j when L = R (A8).
@@ -418,7 +453,7 @@ struct Oracle {
         auto& B = levels[R];
         for (size_t i = 0; i < A.size() && !stop(); ++i)
           for (size_t j = (L == R ? i + 1 : 0); j < B.size() && !stop(); ++j)
-            emit(op_union(A[i].cs, B[j].cs), Prov{K_UNION, L, (long)i, R, (long)j});
+            emit(op_union(A[i].cs, B[j].cs), Prov{K_UNION, L, (uint32_t)i, R, (uint32_t)j});
       }
       st.cand_u = cand_level;
       (void)stop_emitting;
@@ -454,42 +489,134 @@ struct Oracle {
     }
     return done(2);
   }
+
+  // ---- the ABI's view (8-word CSs in and out) -------------------------------
+  static CS from8(const uint64_t* a) {
+    CS x = zero_cs();
+    for (int k = 0; k < W; ++k) x[k] = a ? a[k] : 0;
+    return x;
+  }
+  static void to8(const CS& x, uint64_t* out) {
+    for (int k = 0; k < kMaxWords; ++k) out[k] = k < W ? x[k] : 0;
+  }
+  const std::string& ic_word(int k) const override { return ic.at(k); }
+  const std::vector<std::pair<int, int>>& gt_row(int w) const override { return gt.at(w); }
+  void masks8(uint64_t* pos8, uint64_t* neg8) const override {
+    to8(pos_mask, pos8);
+    to8(neg_mask, neg8);
+  }
+  // op 0 union, 1 concat, 2 star(a), 3 question(a), 4 satisfies(a) (out[0] = 0/1)
+  void op8(int op, const uint64_t* a, const uint64_t* b, uint64_t* out) const override {
+    CS x = from8(a), y = from8(b), r = zero_cs();
+    switch (op) {
+      case 0: r = op_union(x, y); break;
+      case 1: r = op_concat(x, y); break;
+      case 2: r = op_star(x); break;
+      case 3: r = op_question(x); break;
+      case 4: r[0] = satisfies(x) ? 1 : 0; break;
+    }
+    to8(r, out);
+  }
+  int run(int max_cost, long en, long ed, bool cfl, uint64_t me, bool otf_mode) override {
+    err_num = en;
+    err_den = ed > 0 ? ed : 1;
+    complete_final_level = cfl;
+    max_entries = me;
+    onthefly = otf_mode;
+    return solve(max_cost);
+  }
+  int otf() const override { return otf_level; }
+  void result6(long long* out6, double* secs) const override {
+    out6[0] = result_cost;
+    out6[1] = status;
+    out6[2] = (long long)candidates;
+    out6[3] = (long long)cand_complete;
+    out6[4] = last_complete_cost;
+    out6[5] = (long long)n_entries;
+    *secs = seconds;
+  }
+  const std::string& regex_text() const override { return regex; }
+  const std::vector<LevelStat>& level_stats() const override { return stats; }
+  long level_size(int cost) const override {
+    auto it = levels.find(cost);
+    return it == levels.end() ? 0 : (long)it->second.size();
+  }
+  long level_cs8(int cost, uint64_t* out, long cap) const override {
+    auto it = levels.find(cost);
+    if (it == levels.end()) return 0;
+    long m = (long)it->second.size();
+    for (long i = 0; i < m && i < cap; ++i) to8(it->second[i].cs, out + i * kMaxWords);
+    return m;
+  }
+  std::string entry_regex(int cost, long i) const override {
+    return print(levels.at(cost).at(i).prov);
+  }
 };
+
+template <int W>
+Search* make_oracle(const char* alphabet, const char* const* P, int nP, const char* const* N,
+                    int nN, const int* costs5, std::string* err, int* n_out) {
+  auto* o = new Oracle<W>();
+  o->alphabet = alphabet;
+  for (int i = 0; i < nP; ++i) o->P.push_back(P[i]);
+  for (int i = 0; i < nN; ++i) o->N.push_back(N[i]);
+  for (int k = 0; k < 5; ++k) o->c[k] = costs5[k];
+  if (!o->validate()) {
+    *err = o->err;
+    delete o;
+    return nullptr;
+  }
+  // build_ic sets bits of the masks: it needs |IC| <= 64 W (checked first).
+  {
+    std::vector<std::string> all;
+    for (auto* S : {&o->P, &o->N})
+      for (auto& w : *S)
+        for (size_t i = 0; i <= w.size(); ++i)
+          for (size_t j = i; j <= w.size(); ++j) all.push_back(w.substr(i, j - i));
+    std::sort(all.begin(), all.end());
+    all.erase(std::unique(all.begin(), all.end()), all.end());
+    *n_out = (int)all.size();
+    if (*n_out > 64 * W) {
+      delete o;
+      return nullptr;
+    }
+  }
+  o->build_ic();
+  return o;
+}
 
 }  // namespace
 
 // ============================ C ABI for ctypes ================================
 extern "C" {
 
+// The CS width W is the smallest of 1, 2, 4, 8 words holding |IC| bits.
 void* orc_create(const char* alphabet, const char* const* P, int nP, const char* const* N,
                  int nN, const int* costs5, char* errbuf, int errlen) {
-  auto* o = new Oracle();
-  o->alphabet = alphabet;
-  for (int i = 0; i < nP; ++i) o->P.push_back(P[i]);
-  for (int i = 0; i < nN; ++i) o->N.push_back(N[i]);
-  for (int k = 0; k < 5; ++k) o->c[k] = costs5[k];
-  if (!o->validate()) {
-    if (errbuf && errlen > 0) { strncpy(errbuf, o->err.c_str(), errlen - 1); errbuf[errlen - 1] = 0; }
+  std::string err;
+  int n = 0;
+  Search* o = make_oracle<8>(alphabet, P, nP, N, nN, costs5, &err, &n);
+  if (o && n <= 64 * 4) {
     delete o;
-    return nullptr;
+    if (n <= 64) o = make_oracle<1>(alphabet, P, nP, N, nN, costs5, &err, &n);
+    else if (n <= 128) o = make_oracle<2>(alphabet, P, nP, N, nN, costs5, &err, &n);
+    else o = make_oracle<4>(alphabet, P, nP, N, nN, costs5, &err, &n);
   }
-  o->build_ic();
-  if (o->n() > kMaxWords * 64) {
-    if (errbuf && errlen > 0) { strncpy(errbuf, "|IC| > 512", errlen - 1); errbuf[errlen - 1] = 0; }
-    delete o;
-    return nullptr;
+  if (!o && err.empty()) err = "|IC| > 512";
+  if (!o && errbuf && errlen > 0) {
+    strncpy(errbuf, err.c_str(), errlen - 1);
+    errbuf[errlen - 1] = 0;
   }
   return o;
 }
 
-void orc_destroy(void* h) { delete static_cast<Oracle*>(h); }
+void orc_destroy(void* h) { delete static_cast<Search*>(h); }
 
-int orc_n(void* h) { return static_cast<Oracle*>(h)->n(); }
+int orc_n(void* h) { return static_cast<Search*>(h)->n(); }
 
 // Copies IC word k into buf (NUL-terminated); returns its length.
 int orc_ic_word(void* h, int k, char* buf, int buflen) {
-  auto* o = static_cast<Oracle*>(h);
-  const std::string& w = o->ic.at(k);
+  const std::string& w = static_cast<Search*>(h)->ic_word(k);
   int len = (int)w.size();
   if (buf && buflen > len) { memcpy(buf, w.data(), len); buf[len] = 0; }
   return len;
@@ -497,8 +624,7 @@ int orc_ic_word(void* h, int k, char* buf, int buflen) {
 
 // Guide-table row of word w: writes up to cap (l, r) pairs; returns row length.
 int orc_gt_row(void* h, int w, int* pairs, int cap) {
-  auto* o = static_cast<Oracle*>(h);
-  auto& row = o->gt.at(w);
+  auto& row = static_cast<Search*>(h)->gt_row(w);
   for (int k = 0; k < (int)row.size() && k < cap; ++k) {
     pairs[2 * k] = row[k].first;
     pairs[2 * k + 1] = row[k].second;
@@ -507,89 +633,55 @@ int orc_gt_row(void* h, int w, int* pairs, int cap) {
 }
 
 void orc_masks(void* h, uint64_t* pos8, uint64_t* neg8) {
-  auto* o = static_cast<Oracle*>(h);
-  for (int k = 0; k < kMaxWords; ++k) { pos8[k] = o->pos_mask[k]; neg8[k] = o->neg_mask[k]; }
+  static_cast<Search*>(h)->masks8(pos8, neg8);
 }
 
 // CS operations on 8-word CSs: op 0 union, 1 concat, 2 star(a), 3 question(a),
 // 4 satisfies(a) (out[0] = 0/1).
 void orc_op(void* h, int op, const uint64_t* a, const uint64_t* b, uint64_t* out) {
-  auto* o = static_cast<Oracle*>(h);
-  CS x, y, r = zero_cs();
-  for (int k = 0; k < kMaxWords; ++k) { x[k] = a[k]; y[k] = b ? b[k] : 0; }
-  switch (op) {
-    case 0: r = o->op_union(x, y); break;
-    case 1: r = o->op_concat(x, y); break;
-    case 2: r = o->op_star(x); break;
-    case 3: r = o->op_question(x); break;
-    case 4: r[0] = o->satisfies(x) ? 1 : 0; break;
-  }
-  for (int k = 0; k < kMaxWords; ++k) out[k] = r[k];
+  static_cast<Search*>(h)->op8(op, a, b, out);
 }
 
 int orc_solve(void* h, int max_cost, long err_num, long err_den, int complete_final_level,
               unsigned long long max_entries, int onthefly) {
-  auto* o = static_cast<Oracle*>(h);
-  o->err_num = err_num;
-  o->err_den = err_den > 0 ? err_den : 1;
-  o->complete_final_level = complete_final_level != 0;
-  o->max_entries = max_entries;
-  o->onthefly = onthefly != 0;
-  return o->solve(max_cost);
+  return static_cast<Search*>(h)->run(max_cost, err_num, err_den, complete_final_level != 0,
+                                      max_entries, onthefly != 0);
 }
 
-int orc_otf_level(void* h) { return static_cast<Oracle*>(h)->otf_level; }
+int orc_otf_level(void* h) { return static_cast<Search*>(h)->otf(); }
 
-// result: cost, status, candidates (through found), cand_complete, last_complete_cost, seconds
+// result: cost, status, candidates (through found), cand_complete, last_complete_cost, entries
 void orc_result(void* h, long long* out6, double* seconds) {
-  auto* o = static_cast<Oracle*>(h);
-  out6[0] = o->result_cost;
-  out6[1] = o->status;
-  out6[2] = (long long)o->candidates;
-  out6[3] = (long long)o->cand_complete;
-  out6[4] = o->last_complete_cost;
-  out6[5] = (long long)o->n_entries;
-  *seconds = o->seconds;
+  static_cast<Search*>(h)->result6(out6, seconds);
 }
 
 int orc_regex(void* h, char* buf, int buflen) {
-  auto* o = static_cast<Oracle*>(h);
-  int len = (int)o->regex.size();
-  if (buf && buflen > len) { memcpy(buf, o->regex.data(), len); buf[len] = 0; }
+  const std::string& r = static_cast<Search*>(h)->regex_text();
+  int len = (int)r.size();
+  if (buf && buflen > len) { memcpy(buf, r.data(), len); buf[len] = 0; }
   return len;
 }
 
-int orc_num_stats(void* h) { return (int)static_cast<Oracle*>(h)->stats.size(); }
+int orc_num_stats(void* h) { return (int)static_cast<Search*>(h)->level_stats().size(); }
 
 // stat k: cost, cand_q, cand_s, cand_c, cand_u, unique, complete
 void orc_stat(void* h, int k, unsigned long long* out7) {
-  auto& s = static_cast<Oracle*>(h)->stats.at(k);
+  auto& s = static_cast<Search*>(h)->level_stats().at(k);
   out7[0] = s.cost; out7[1] = s.cand_q; out7[2] = s.cand_s; out7[3] = s.cand_c;
   out7[4] = s.cand_u; out7[5] = s.unique; out7[6] = s.complete;
 }
 
 // Number of cached entries at cost level c (0 if none).
-long orc_level_size(void* h, int cost) {
-  auto* o = static_cast<Oracle*>(h);
-  auto it = o->levels.find(cost);
-  return it == o->levels.end() ? 0 : (long)it->second.size();
-}
+long orc_level_size(void* h, int cost) { return static_cast<Search*>(h)->level_size(cost); }
 
 // Copies the CSs of level c (8 words each) into out (cap entries).
 long orc_level_cs(void* h, int cost, uint64_t* out, long cap) {
-  auto* o = static_cast<Oracle*>(h);
-  auto it = o->levels.find(cost);
-  if (it == o->levels.end()) return 0;
-  long m = (long)it->second.size();
-  for (long i = 0; i < m && i < cap; ++i)
-    for (int k = 0; k < kMaxWords; ++k) out[i * kMaxWords + k] = it->second[i].cs[k];
-  return m;
+  return static_cast<Search*>(h)->level_cs8(cost, out, cap);
 }
 
 // Regex of cached entry i at level c (reconstruction audit).
 int orc_entry_regex(void* h, int cost, long i, char* buf, int buflen) {
-  auto* o = static_cast<Oracle*>(h);
-  std::string s = o->print(o->levels.at(cost).at(i).prov);
+  std::string s = static_cast<Search*>(h)->entry_regex(cost, i);
   int len = (int)s.size();
   if (buf && buflen > len) { memcpy(buf, s.data(), len); buf[len] = 0; }
   return len;
