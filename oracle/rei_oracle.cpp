@@ -41,6 +41,8 @@
 #include <array>
 #include <chrono>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -484,6 +486,12 @@ struct Oracle : Search {
       if (oom) return done(3);
       cand_complete = candidates;
       last_complete_cost = cost;
+      if (std::getenv("ORACLE_PROGRESS") && (st.cand_q + st.cand_s + st.cand_c + st.cand_u))
+        std::fprintf(stderr, "[oracle] level %d unique %llu cand %llu entries %llu %.1f s\n", cost,
+                     (unsigned long long)st.unique,
+                     (unsigned long long)(st.cand_q + st.cand_s + st.cand_c + st.cand_u),
+                     (unsigned long long)n_entries,
+                     std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
       break;
      }
     }

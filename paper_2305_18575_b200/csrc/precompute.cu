@@ -85,6 +85,10 @@ __global__ void k_tables(const unsigned long long* __restrict__ ic, const int* _
   __shared__ int s_maxk, s_maxlen;
   __shared__ uint32_t s_pos[kMaxW32], s_neg[kMaxW32];
   const int n = *n_ptr;
+  if (n > kMaxNW) {  // |IC| > 512: the host rejects the spec (REI_EINVAL); index no table
+    if (threadIdx.x == 0) { out->n = n; out->maxk = 0; out->maxlen = 0; out->bad = 0; }
+    return;
+  }
   if (threadIdx.x == 0) { s_maxk = 0; s_maxlen = 0; }
   if (threadIdx.x < kMaxW32) { s_pos[threadIdx.x] = 0; s_neg[threadIdx.x] = 0; }
   __syncthreads();

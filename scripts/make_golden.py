@@ -26,6 +26,10 @@ SPECS = {
     "c1_toy": (specgen.C1_TOY, 20),
     "e1": (specgen.E1, 20),
     "intro": (specgen.INTRO, 20),
+    # BASELINE configs[1]: Type 1, binary, le = 6, p = n = 10, seed 0
+    "c2_t1_s0": (specgen.gen_type1("01", 6, 10, 10, 0), 40),
+    # BASELINE configs[3]: 4 symbols, planted target (DESIGN.md input recipe), |IC| = 148
+    "c4_planted_s0": (specgen.gen_planted("abcd", "(a+b+c)*d(a+c)(b+d)", 10, 10, 4, 8, 0), 40),
 }
 
 
@@ -33,12 +37,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("name", choices=sorted(SPECS))
     ap.add_argument("--max-cost", type=int, default=None)
+    ap.add_argument("--stop-at-first", action="store_true",
+                    help="stop at the first precise candidate (do not finish level c*)")
     args = ap.parse_args()
     spec, mc = SPECS[args.name]
     mc = args.max_cost or mc
     t0 = time.time()
     o = oracle.Oracle.from_spec(spec)
-    r = o.solve(mc, complete_final_level=True)
+    r = o.solve(mc, complete_final_level=not args.stop_at_first)
     out = {
         "spec": {"alphabet": spec.alphabet, "P": list(spec.P), "N": list(spec.N),
                  "costs": list(spec.costs), "name": spec.name},
@@ -50,6 +56,7 @@ def main():
         "cstar": r.cost,
         "regex": r.regex,
         "candidates_through_found": r.candidates,
+        "complete_final_level": not args.stop_at_first,
         "levels": [
             {"cost": l.cost, "unique": l.unique, "cand_q": l.cand_q, "cand_s": l.cand_s,
              "cand_c": l.cand_c, "cand_u": l.cand_u, "complete": l.complete}

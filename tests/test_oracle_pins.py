@@ -157,6 +157,10 @@ BRUTE_CASES = [
     (specgen.Spec("01", ("0", "00"), ("1", "")), (1, 1, 1, 1, 1), 7),
     (specgen.Spec("ab", ("ab", "ba", "aa"), ("b", "bb", "")), (1, 1, 1, 1, 1), 7),
     (specgen.Spec("abc", ("abc", "c", "ac"), ("a", "bc", "")), (1, 2, 1, 1, 2), 7),
+    # reading A2: symbol c occurs in no example, so its seed is the empty language
+    # (the brute force matches `c` against IC and finds nothing); it changes the counts
+    (specgen.Spec("abc", ("ab", "ba", "aa"), ("b", "bb", "")), (1, 1, 1, 1, 1), 6),
+    (specgen.Spec("abc", ("a", "aa", "ab"), ("b", "", "ba")), (1, 1, 1, 1, 1), 6),
 ]
 
 
