@@ -44,6 +44,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <map>
 #include <memory>
@@ -141,7 +142,7 @@ struct Oracle : Search {
   CS pos_mask, neg_mask;
 
   // Language cache: levels[c] = unique CSs of minimal cost c, in creation order.
-  std::map<int, std::vector<Entry>> levels;
+  std::map<int, std::deque<Entry>> levels;  // deque: no 2x peak while a level grows
   std::unordered_set<CS, CSHash> seen;
   std::vector<LevelStat> stats;
 
@@ -310,7 +311,7 @@ struct Oracle : Search {
 
   // ---- Algorithm 1 --------------------------------------------
   uint64_t cand_level = 0;
-  std::vector<Entry>* cur = nullptr;
+  std::deque<Entry>* cur = nullptr;
   bool found = false;
   Prov found_prov{};
   bool oom = false;
@@ -411,7 +412,7 @@ struct Oracle : Search {
      if (needs_uncached(cost)) return done(3);  // OnTheFly ran out of cached operands
      const uint64_t cand_before = candidates, entries_before = n_entries;
      for (int attempt = 0; attempt < 2; ++attempt) {
-      std::vector<Entry> fresh;
+      std::deque<Entry> fresh;
       cur = &fresh;
       LevelStat st{cost, 0, 0, 0, 0, 0, 0};
       bool stop_emitting = false;
