@@ -216,14 +216,8 @@ def run_ours(args, rank, world, local_rank):
         dist.broadcast_object_list(box, src=0)
         mkw = dict(world_size=world, rank=rank, nccl_id=box[0])
     multi_note = None
-    try:
-        solver = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw)
-    except Exception as e:  # noqa: BLE001 -- recorded in the JSON line, never silent
-        if not sharded:
-            raise
-        multi_note = f"sharded init failed ({e}); ran independent replicas instead"
-        sharded = False
-        solver = Solver.from_spec(spec, device=local_rank, stream=stream)
+    # no fallback: a failing multi-GPU init or solve raises (and the run fails)
+    solver = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw)
     # L2 flush buffer (> 126 MB L2), written between timed steps
     flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
 
@@ -231,21 +225,9 @@ def run_ours(args, rank, world, local_rank):
         if world > 1:
             dist.barrier()
 
-    try:
-        for _ in range(args.warmup):
-            r = solver.solve(max_cost)
-            assert r.status == "found", r.status
-    except Exception as e:  # noqa: BLE001 -- recorded in the JSON line, never silent
-        if not sharded:
-            raise
-        # the sharded transport failed on this box (every rank sees the collective fail):
-        # fall back to independent replicas and say so
-        multi_note = f"sharded solve failed ({e}); ran independent replicas instead"
-        sharded = False
-        solver = Solver.from_spec(spec, device=local_rank, stream=stream)
-        for _ in range(args.warmup):
-            r = solver.solve(max_cost)
-            assert r.status == "found", r.status
+    for _ in range(args.warmup):
+        r = solver.solve(max_cost)
+        assert r.status == "found", r.status
     torch.cuda.synchronize()
     solver.reset_kernel_stats()
     launches0 = solver.launch_count()
@@ -427,7 +409,8 @@ def run_ours(args, rank, world, local_rank):
             "candidates_through_last_complete_level": r0.cand_complete,
             "time_to_minimal_re_ms": statistics.median(step_ms),
             "l2": f"{args.flush_mb} MiB buffer written between timed steps (L2 flush)",
-            "parallelism": (f"shard{world} (level work lists partitioned, NCCL all-gather of new CSs)"
+            "parallelism": (f"shard{world} (level work lists partitioned; hash-owner NCCL all-to-all, "
+                            "owner dedup, all-gather of the uniques)"
                             if sharded else f"replicas{world}") if world > 1 else "single",
             "multi_note": multi_note,
             "paper_context": paper,
@@ -457,9 +440,22 @@ def main():
     ap.add_argument("--multi", choices=["shard", "replicas"], default="shard",
                     help="N > 1: one sharded search (default) or N independent replicas")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `bench.py --gpus N` without a launcher: become N ranks (one process per GPU)
+        # under torch.distributed.run on this node
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        return subprocess.call(cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.gpus != world:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args, rank)
     if world > 1:

@@ -79,11 +79,13 @@ typedef struct {
   /* multi-GPU (one context per rank; rei_solve is then collective, S 8(e)) */
   int world_size;            /* 0 or 1 = single GPU                                       */
   int rank;
-  const void* nccl_unique_id;/* 128-byte ncclUniqueId, broadcast by the caller (rank 0's) */
+  const void* nccl_unique_id;/* 128-byte ncclUniqueId, broadcast by the caller (rank 0's);
+                                NULL with `allgather` set: host-staged level exchange      */
   uint64_t max_entries;      /* cap on cached CSs (the language cache size); 0 = set by the
                                 memory budget only.  With REI_FLAG_SHARDED_CACHE: per rank  */
-  rei_allgather_fn allgather;/* REI_FLAG_SHARDED_CACHE, one process per rank: the host
-                                all-gather (NULL otherwise; nccl_unique_id is then unused) */
+  rei_allgather_fn allgather;/* one process per rank: the host all-gather used by
+                                REI_FLAG_SHARDED_CACHE, and by the replicated multi-rank
+                                search when nccl_unique_id is NULL (NULL otherwise)        */
   void* allgather_user;      /* passed back to `allgather`                                */
 } rei_options;
 
@@ -189,15 +191,24 @@ rei_status rei_entry_regex(const void* ctx, uint32_t cost, uint64_t i, char* buf
 rei_status rei_cs_ops(void* ctx, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                       size_t count);
 
-/* ---- multi-GPU: the sharded level ----
- * Every rank holds the full language cache.  Each level's work lists (? and *
- * operands, concatenation and union work items) are split into contiguous rank
- * shares (rei_partition); a rank enumerates its share, appends the CSs new to its
- * dedup set, and the ranks' lists are all-gathered in rank order; every rank then
- * keeps the first occurrence of each CS (canonical merge), so the caches stay
- * byte-identical.  found / overflow / counts are combined over all ranks.
- * Supported for |IC| <= 64 (bitmap and 64-bit-key dedup sets). */
-
+/* ---- multi-GPU: the sharded level (north_star "Multi-GPU partition") ----
+ * Every rank holds the full language cache (replicated: speed, not capacity).  A
+ * level with fewer than REI_REDUNDANT_CAND candidates (default 5e7; |IC| <= 64) runs
+ * whole on every rank and is then sorted by CS into a rank-independent order.  A
+ * larger level is split: each of its work lists (? and * operands, concatenation and
+ * union work items, the paper's pair space P:977-978) is cut into contiguous rank
+ * shares (rei_partition); a rank probes its full replica for every candidate of its
+ * share and stages the CSs new to it.  The exchange then (1) buckets the staged CSs
+ * by hash owner (rei_cs_owner), (2) sends each bucket to its owner (NCCL grouped
+ * send/recv all-to-all), (3) the owner keeps one copy of each CS, (4) the owners'
+ * unique lists are all-gathered in owner order into every rank's arena and inserted
+ * into its dedup set; the precise-candidate rank is min-reduced with the level's
+ * control lines.  Every rank ends each level with byte-identical caches, so later
+ * candidate ranks name the same operands everywhere.  Any |IC| <= 512.
+ * Transports: NCCL (one process per GPU, rei_options.nccl_unique_id), the caller's
+ * host all-gather callback (rei_options.allgather with nccl_unique_id NULL: a
+ * host-staged exchange, e.g. torch.distributed gloo), or device peer copies
+ * (virtual ranks, rei_solve_group). */
 /* One process per GPU: rank 0 creates the id, the caller broadcasts it (e.g. with
  * torch.distributed) and passes it in rei_options.nccl_unique_id with world_size and
  * rank; rei_init and rei_solve are then collective over the world. out: 128 bytes. */
@@ -233,6 +244,16 @@ rei_status rei_solve_batch(void* const* ctxs, size_t n, uint32_t max_cost, int t
 
 /* ---- multi-GPU host logic (pure functions, usable without a GPU) ---- */
 
+/* Hash owner of a CS (cs_words 32-bit words, LSB-first as everywhere) among `world`
+ * ranks: the rank that deduplicates it in the level exchange (and owns it in the
+ * sharded cache).  The level kernels use the same function.  -1 for a bad width. */
+int rei_cs_owner(const uint32_t* cs, uint32_t cs_words, int world);
+/* Offsets of the level exchange's all-to-all for `rank`, given the world x world
+ * matrix counts[src * world + dst] of records rank src sends to rank dst:
+ * send_off[o] = first record of the bucket for o in rank's send list (buckets in
+ * owner order); recv_off[r] = first record from source r in rank's receive list
+ * (sources in rank order).  Either output may be NULL. */
+void rei_exchange_offsets(int world, const uint64_t* counts, int rank, uint64_t* send_off, uint64_t* recv_off);
 /* Contiguous share of a flattened candidate / work-item space of size `total` for
  * rank g of G: [*begin, *end) (S 8(e) "Partition"). */
 void rei_partition(uint64_t total, int G, int g, uint64_t* begin, uint64_t* end);

@@ -89,17 +89,6 @@ __device__ __forceinline__ bool cs_equal(const uint32_t (&a)[W], const uint32_t 
   return d == 0;
 }
 
-template <int W>
-__device__ __forceinline__ unsigned long long hash_cs(const uint32_t (&cs)[W]) {
-  unsigned long long h = 0x9E3779B97F4A7C15ull;
-#pragma unroll
-  for (int q = 0; q < W; ++q) {
-    h = (h ^ cs[q]) * 0xBF58476D1CE4E5B9ull;
-    h ^= h >> 31;
-  }
-  h *= 0x94D049BB133111EBull;
-  return h ^ (h >> 29);
-}
 
 template <int W>
 __device__ __forceinline__ void load_cs(const uint32_t* __restrict__ arena, uint64_t idx, uint32_t (&x)[W]) {
@@ -153,12 +142,32 @@ __device__ __forceinline__ void append(const LevelParams& p, const uint32_t (&cs
 
 // ---- dedup: indexed hash set for wide CSs (fingerprint + arena index).
 // Slot = (fp << 32) | idx, 0 = empty, idx == kLocked while the owner writes the CS.
+// Multi-rank levels (p.tent = kTent) append to a staging list instead of the arena:
+// their slots carry idx = kTent | staging index ("tentative"), and the CS is compared
+// from p.stage_cs.  After the level exchange, k_rehash (do_append = false) re-points
+// each tentative slot whose key is in the exchanged level to its arena index.
 // `S` is LevelParams (the local cache) or Peer (the owner's cache, sharded mode).
+constexpr uint32_t kTent = 0x80000000u;
+constexpr uint32_t kDead = 0xfffffffeu;
+template <class S>
+__device__ __forceinline__ const uint32_t* stage_of(const S& p) { return nullptr; }
+template <>
+__device__ __forceinline__ const uint32_t* stage_of<LevelParams>(const LevelParams& p) { return p.stage_cs; }
+template <class S>
+__device__ __forceinline__ const uint32_t* arena_of(const S& p) { return p.arena_out; }
+template <>
+__device__ __forceinline__ const uint32_t* arena_of<LevelParams>(const LevelParams& p) { return p.arena; }
+template <class S>
+__device__ __forceinline__ uint32_t tent_of(const S& p) { return 0u; }
+template <>
+__device__ __forceinline__ uint32_t tent_of<LevelParams>(const LevelParams& p) { return p.tent; }
+
 template <int W, class S>
 __device__ bool insert_indexed(const S& p, const uint32_t (&cs)[W], unsigned long long rank,
                                bool do_append, unsigned long long known_idx) {
   const unsigned long long h = hash_cs<W>(cs);
   const uint32_t fp = (uint32_t)(h >> 32) | 1u;
+  const uint32_t tent = do_append ? tent_of(p) : 0u;
   unsigned long long s = h & p.dedup.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     // the level already overflowed: it will be redone after growth -- stop inserting
@@ -171,16 +180,16 @@ __device__ bool insert_indexed(const S& p, const uint32_t (&cs)[W], unsigned lon
         unsigned long long idx = known_idx;
         if (do_append) {
           idx = p.out_base + atomicAdd(&p.ctl->count, 1ull);
-          if (idx >= p.cap || idx >= 0xfffffff0ull) {
+          if (idx >= p.cap || idx >= (tent ? 0x7ffffff0ull : 0xfffffff0ull)) {
             p.ctl->overflow = 1;
-            atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | 0xfffffffeu);  // dead
+            atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | kDead);  // dead
             return false;
           }
           store_cs<W>(p.arena_out, idx, cs);
           p.bp[idx] = rank;
           __threadfence();
         }
-        atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | (uint32_t)idx);
+        atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | ((uint32_t)idx | tent));
         return true;
       }
       v = old;
@@ -191,12 +200,19 @@ __device__ bool insert_indexed(const S& p, const uint32_t (&cs)[W], unsigned lon
         __nanosleep(32);
         idx = (uint32_t)(*(volatile unsigned long long*)&p.dedup.table[s]);
       }
-      if (idx != 0xfffffffeu) {
+      if (idx != kDead) {
+        const bool tentative = (idx & kTent) != 0;
+        const uint32_t* base = tentative ? stage_of(p) : arena_of(p);
         uint32_t other[W];
-        const volatile uint32_t* src = p.arena_out + (unsigned long long)idx * W;
+        const volatile uint32_t* src = base + (unsigned long long)(idx & ~(tentative ? kTent : 0u)) * W;
 #pragma unroll
         for (int q = 0; q < W; ++q) other[q] = src[q];
-        if (cs_equal<W>(cs, other)) return false;
+        if (cs_equal<W>(cs, other)) {
+          // the exchanged level's arena entry takes over a tentative (staged) slot
+          if (!do_append && tentative)
+            atomicExch(&p.dedup.table[s], ((unsigned long long)fp << 32) | (uint32_t)known_idx);
+          return false;
+        }
       }
     }
     s = (s + 1) & p.dedup.mask;

@@ -44,6 +44,8 @@ struct NcclApi {
   ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 NcclApi& nccl_api() {
@@ -66,8 +68,10 @@ NcclApi& nccl_api() {
   a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(dlsym(h, "ncclBroadcast"));
   a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
   a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+  a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+  a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
   a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.Broadcast && a.GroupStart &&
-         a.GroupEnd;
+         a.GroupEnd && a.Send && a.Recv;
   return a;
 }
 }  // namespace
@@ -185,10 +189,14 @@ struct Ctx {
   // multi-rank
   int world = 1, rank = 0;
   void* nccl = nullptr;              // ncclComm_t (one process per GPU)
+  bool host_xport = false;           // exchange through the caller's allgather callback
   LevelCtl* d_ctl_all = nullptr;     // [world] gathered control lines
-  uint32_t* g_cs = nullptr;          // gathered new-CS lists of a level
-  unsigned long long* g_bp = nullptr;
-  uint64_t gather_cap = 0;
+  unsigned long long* d_small = nullptr;      // [64] small all-gather send (NCCL)
+  unsigned long long* d_small_all = nullptr;  // [world * 64]
+  uint32_t* st_cs = nullptr;         // staging list of an exchanged level (this rank's new CSs)
+  unsigned long long* st_bp = nullptr;
+  uint64_t st_cap = 0;
+  XScratch xs;
   MergeScratch merge;
 
   // profiling
@@ -218,13 +226,15 @@ struct Ctx {
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (void* q : {(void*)arena, (void*)bp, (void*)tarena, (void*)bitmap, (void*)table, (void*)special,
                     (void*)ctl_base, (void*)d_blocks, (void*)d_peers, (void*)tab.split, (void*)tab.nsplit,
-                    (void*)tab.word_len, (void*)tab.seeds, (void*)d_ctl_all, (void*)g_cs, (void*)g_bp})
+                    (void*)tab.word_len, (void*)tab.seeds, (void*)d_ctl_all, (void*)st_cs, (void*)st_bp,
+                    (void*)d_small, (void*)d_small_all})
       dfree(q);
     host_free(h_peers);
     host_free(h_ctl);
     host_free(h_blocks);
     for (auto e : ev_pool) cudaEventDestroy(e);
     free_merge_scratch(merge);
+    free_xscratch(xs);
     if (nccl) nccl_api().CommDestroy((ncclComm_t)nccl);
     if (stream) cudaStreamSynchronize(stream);  // the pooled frees above are stream-ordered
     for (int i = 0; i < 3; ++i) {
@@ -666,13 +676,15 @@ rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
 }
 
 // Multi-rank transport of the sharded level.  `m` holds the ranks
-// driven by this process: all `world` ranks (virtual ranks, rei_solve_group) or
-// exactly one (one process per GPU; the exchange goes through NCCL).
+// driven by this process: all `world` ranks (virtual ranks, rei_solve_group: device /
+// peer copies) or exactly one (one process per GPU: NCCL, or -- host_xport -- the
+// caller's host all-gather callback, e.g. torch.distributed gloo).
 struct Comm {
   int world = 1;
   int rank0 = 0;
   std::vector<Ctx*> m;
   void* nccl = nullptr;  // ncclComm_t of m[0] when each process holds one rank
+  bool host = false;     // one rank per process, exchanging through m[0]->allgather
 };
 
 void reset_search(Ctx* c) {
@@ -687,14 +699,23 @@ void reset_search(Ctx* c) {
   c->result.cs_words = (uint32_t)c->W32;
 }
 
+rei_status host_allgather(Ctx* c, const void* send, void* recv, size_t bytes, const char* what) {
+  if (c->allgather(c->allgather_user, send, recv, bytes) != 0) {
+    c->err = std::string("allgather callback failed (") + what + ")";
+    return REI_ENCCL;
+  }
+  return REI_OK;
+}
+
 // Every rank's control line, in rank order, on every member.
 rei_status gather_ctl(Comm& g, std::vector<LevelCtl>& all) {
   all.assign(g.world, LevelCtl{});
-  if (!g.nccl) {
+  if (!g.nccl && !g.host) {
     for (size_t i = 0; i < g.m.size(); ++i) all[g.rank0 + i] = *g.m[i]->h_ctl;
     return REI_OK;
   }
   Ctx* c = g.m[0];
+  if (g.host) return host_allgather(c, c->h_ctl, all.data(), sizeof(LevelCtl), "level control");
   if (nccl_api().AllGather(c->ctl, c->d_ctl_all, sizeof(LevelCtl), ncclUint8, (ncclComm_t)g.nccl, c->stream) !=
       ncclSuccess) {
     c->err = "ncclAllGather(level control) failed";
@@ -707,94 +728,272 @@ rei_status gather_ctl(Comm& g, std::vector<LevelCtl>& all) {
   return REI_OK;
 }
 
-rei_status ensure_gather(Ctx* c, uint64_t m) {
-  if (c->gather_cap >= m) return REI_OK;
-  c->dfree(c->g_cs);
-  c->dfree(c->g_bp);
-  c->g_cs = nullptr;
-  c->g_bp = nullptr;
-  const uint64_t cap = std::max<uint64_t>(m, 2 * c->gather_cap);
-  CUDA_OK(c, c->dmalloc(&c->g_cs, cap * 4ull * c->W32));
-  CUDA_OK(c, c->dmalloc(&c->g_bp, cap * 8ull));
-  c->gather_cap = cap;
+// All-gather of k host u64 per rank: out[r * k + j] = rank r's value j.
+rei_status x_gather_u64(Comm& g, const std::vector<std::vector<uint64_t>>& mine, size_t k,
+                        std::vector<uint64_t>& out) {
+  out.assign((size_t)g.world * k, 0);
+  if (!g.nccl && !g.host) {
+    for (size_t i = 0; i < g.m.size(); ++i)
+      std::copy(mine[i].begin(), mine[i].begin() + k, out.begin() + (g.rank0 + i) * k);
+    return REI_OK;
+  }
+  Ctx* c = g.m[0];
+  if (g.host) return host_allgather(c, mine[0].data(), out.data(), k * 8, "counts");
+  if (k > 64) { c->err = "x_gather_u64: k > 64"; return REI_EINVAL; }
+  CUDA_OK(c, cudaMemcpyAsync(c->d_small, mine[0].data(), k * 8, cudaMemcpyHostToDevice, c->stream));
+  if (nccl_api().AllGather(c->d_small, c->d_small_all, k * 8, ncclUint8, (ncclComm_t)g.nccl, c->stream) !=
+      ncclSuccess) {
+    c->err = "ncclAllGather(counts) failed";
+    return REI_ENCCL;
+  }
+  CUDA_OK(c, cudaMemcpyAsync(out.data(), c->d_small_all, (size_t)g.world * k * 8, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->h2d_bytes += k * 8;
+  c->d2h_bytes += (size_t)g.world * k * 8;
   return REI_OK;
 }
 
-// All-gather the ranks' new-CS lists of the level (in rank order) and replace each
-// member's level with the canonical first-occurrence merge.  Returns its size.
-rei_status exchange_level(Comm& g, uint64_t begin, const std::vector<LevelCtl>& all, uint64_t* out_count) {
-  std::vector<uint64_t> off(g.world + 1, 0);
-  for (int r = 0; r < g.world; ++r) off[r + 1] = off[r] + all[r].count;
-  const uint64_t M = off[g.world];
-  uint64_t canon = ~0ull;
-  // 1) gather every rank's list into every member (all gathers complete before any
-  //    member overwrites its level with the merge: the lists are read in place)
-  for (size_t i = 0; i < g.m.size(); ++i) {
-    Ctx* c = g.m[i];
-    rei_status s = ensure_gather(c, M);
-    if (s != REI_OK) return s;
-    const size_t csb = 4ull * c->W32;
-    if (!g.nccl) {
-      for (int r = 0; r < g.world; ++r) {
-        Ctx* src = g.m[r - g.rank0];
-        if (!all[r].count) continue;
-        CUDA_OK(c, cudaMemcpyPeerAsync(c->g_cs + off[r] * c->W32, c->device, src->arena + begin * c->W32,
-                                       src->device, all[r].count * csb, c->stream));
-        CUDA_OK(c, cudaMemcpyPeerAsync(c->g_bp + off[r], c->device, src->bp + begin, src->device,
-                                       all[r].count * 8ull, c->stream));
-      }
-    } else {
-      const int me = g.rank0;
-      nccl_api().GroupStart();
-      for (int r = 0; r < g.world; ++r) {
-        if (!all[r].count) continue;
-        nccl_api().Broadcast(r == me ? (const void*)(c->arena + begin * c->W32) : nullptr, c->g_cs + off[r] * c->W32,
-                      all[r].count * c->W32, ncclUint32, r, (ncclComm_t)g.nccl, c->stream);
-        nccl_api().Broadcast(r == me ? (const void*)(c->bp + begin) : nullptr, c->g_bp + off[r], all[r].count,
-                      ncclUint64, r, (ncclComm_t)g.nccl, c->stream);
-      }
-      if (nccl_api().GroupEnd() != ncclSuccess) {
-        c->err = "NCCL all-gather of the level lists failed";
-        return REI_ENCCL;
+// All-to-all of variable-size record buckets: rank r sends cnt[r][o] records from
+// send[r] + soff(r, o) to rank o, which receives them at recv[o] + roff(o, r)
+// (sources in rank order).  send / recv are indexed by member.
+rei_status x_alltoallv(Comm& g, const std::vector<const uint8_t*>& send, const std::vector<uint8_t*>& recv,
+                       const std::vector<uint64_t>& cnt, size_t rec) {
+  const int W = g.world;
+  // offsets of bucket o in rank r's send list / of source r in rank o's receive list
+  std::vector<uint64_t> so((size_t)W * (W + 1)), ro((size_t)W * (W + 1));
+  for (int r = 0; r < W; ++r) {
+    rei_exchange_offsets(W, cnt.data(), r, &so[(size_t)r * (W + 1)], &ro[(size_t)r * (W + 1)]);
+    so[(size_t)r * (W + 1) + W] = so[(size_t)r * (W + 1) + W - 1] + cnt[(size_t)r * W + W - 1];
+    ro[(size_t)r * (W + 1) + W] = ro[(size_t)r * (W + 1) + W - 1] + cnt[(size_t)(W - 1) * W + r];
+  }
+  auto soff = [&](int r, int o) { return so[(size_t)r * (W + 1) + o]; };
+  auto roff = [&](int o, int r) { return ro[(size_t)o * (W + 1) + r]; };
+  if (!g.nccl && !g.host) {
+    for (Ctx* c : g.m) CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < g.m.size(); ++i) {        // destination
+      Ctx* d = g.m[i];
+      const int o = g.rank0 + (int)i;
+      for (size_t j = 0; j < g.m.size(); ++j) {      // source
+        const int r = g.rank0 + (int)j;
+        const uint64_t n = cnt[(size_t)r * W + o];
+        if (!n) continue;
+        CUDA_OK(d, cudaMemcpyPeerAsync(recv[i] + roff(o, r) * rec, d->device, send[j] + soff(r, o) * rec,
+                                       g.m[j]->device, n * rec, d->stream));
       }
     }
+    for (Ctx* c : g.m) CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    return REI_OK;
   }
-  for (Ctx* c : g.m) CUDA_OK(c, cudaStreamSynchronize(c->stream));
-  // 2) canonical merge on every member (identical input bytes -> identical output)
-  for (Ctx* c : g.m) {
-    uint64_t cnt = 0;
+  Ctx* c = g.m[0];
+  const int me = g.rank0;
+  if (g.host) {
+    uint64_t maxb = 0;
+    for (int r = 0; r < W; ++r) maxb = std::max<uint64_t>(maxb, soff(r, W) * rec);
+    maxb = std::max<uint64_t>(maxb, 8);
+    std::vector<uint8_t> mine(maxb, 0), all((size_t)W * maxb);
+    if (soff(me, W))
+      CUDA_OK(c, cudaMemcpyAsync(mine.data(), send[0], soff(me, W) * rec, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    rei_status s = host_allgather(c, mine.data(), all.data(), maxb, "level records");
+    if (s != REI_OK) return s;
+    for (int r = 0; r < W; ++r) {
+      const uint64_t n = cnt[(size_t)r * W + me];
+      if (n)
+        CUDA_OK(c, cudaMemcpyAsync(recv[0] + roff(me, r) * rec, all.data() + (size_t)r * maxb + soff(r, me) * rec,
+                                   n * rec, cudaMemcpyHostToDevice, c->stream));
+    }
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    c->d2h_bytes += soff(me, W) * rec;
+    c->h2d_bytes += roff(me, W) * rec;
+    return REI_OK;
+  }
+  // NCCL: grouped point-to-point sends / receives (the self bucket is a local copy)
+  const uint64_t self = cnt[(size_t)me * W + me];
+  if (self)
+    CUDA_OK(c, cudaMemcpyAsync(recv[0] + roff(me, me) * rec, send[0] + soff(me, me) * rec, self * rec,
+                               cudaMemcpyDeviceToDevice, c->stream));
+  nccl_api().GroupStart();
+  for (int o = 0; o < W; ++o) {
+    if (o == me) continue;
+    const uint64_t ns = cnt[(size_t)me * W + o], nr = cnt[(size_t)o * W + me];
+    if (ns) nccl_api().Send(send[0] + soff(me, o) * rec, ns * rec, ncclUint8, o, (ncclComm_t)g.nccl, c->stream);
+    if (nr) nccl_api().Recv(recv[0] + roff(me, o) * rec, nr * rec, ncclUint8, o, (ncclComm_t)g.nccl, c->stream);
+  }
+  if (nccl_api().GroupEnd() != ncclSuccess) {
+    c->err = "NCCL all-to-all of the level records failed";
+    return REI_ENCCL;
+  }
+  return REI_OK;
+}
+
+// All-gather of variable-size record lists: rank r's u[r] records from send[r] land at
+// recv + uoff(r) on every rank (rank order).
+rei_status x_allgatherv(Comm& g, const std::vector<const uint8_t*>& send, const std::vector<uint8_t*>& recv,
+                        const std::vector<uint64_t>& u, size_t rec) {
+  const int W = g.world;
+  std::vector<uint64_t> uoff(W + 1, 0);
+  for (int r = 0; r < W; ++r) uoff[r + 1] = uoff[r] + u[r];
+  if (!g.nccl && !g.host) {
+    for (Ctx* c : g.m) CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < g.m.size(); ++i)
+      for (size_t j = 0; j < g.m.size(); ++j) {
+        const int r = g.rank0 + (int)j;
+        if (!u[r]) continue;
+        CUDA_OK(g.m[i], cudaMemcpyPeerAsync(recv[i] + uoff[r] * rec, g.m[i]->device, send[j], g.m[j]->device,
+                                            u[r] * rec, g.m[i]->stream));
+      }
+    for (Ctx* c : g.m) CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    return REI_OK;
+  }
+  Ctx* c = g.m[0];
+  const int me = g.rank0;
+  if (g.host) {
+    uint64_t maxb = 8;
+    for (int r = 0; r < W; ++r) maxb = std::max<uint64_t>(maxb, u[r] * rec);
+    std::vector<uint8_t> mine(maxb, 0), all((size_t)W * maxb);
+    if (u[me]) CUDA_OK(c, cudaMemcpyAsync(mine.data(), send[0], u[me] * rec, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    rei_status s = host_allgather(c, mine.data(), all.data(), maxb, "level uniques");
+    if (s != REI_OK) return s;
+    for (int r = 0; r < W; ++r)
+      if (u[r])
+        CUDA_OK(c, cudaMemcpyAsync(recv[0] + uoff[r] * rec, all.data() + (size_t)r * maxb, u[r] * rec,
+                                   cudaMemcpyHostToDevice, c->stream));
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    c->d2h_bytes += u[me] * rec;
+    c->h2d_bytes += uoff[W] * rec;
+    return REI_OK;
+  }
+  nccl_api().GroupStart();
+  for (int r = 0; r < W; ++r) {
+    if (!u[r]) continue;
+    nccl_api().Broadcast(r == me ? (const void*)send[0] : nullptr, recv[0] + uoff[r] * rec, u[r] * rec, ncclUint8, r,
+                         (ncclComm_t)g.nccl, c->stream);
+  }
+  if (nccl_api().GroupEnd() != ncclSuccess) {
+    c->err = "NCCL all-gather of the level uniques failed";
+    return REI_ENCCL;
+  }
+  return REI_OK;
+}
+
+// Staging list of a multi-rank level (this rank's locally new CSs), >= n entries.
+rei_status ensure_stage(Ctx* c, uint64_t n) {
+  if (c->st_cap >= n) return REI_OK;
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->dfree(c->st_cs);
+  c->dfree(c->st_bp);
+  c->st_cs = nullptr;
+  c->st_bp = nullptr;
+  const uint64_t cap = std::max<uint64_t>(n, 2 * c->st_cap);
+  c->st_cap = 0;
+  CUDA_OK(c, c->dmalloc(&c->st_cs, cap * 4ull * c->W32));
+  CUDA_OK(c, c->dmalloc(&c->st_bp, cap * 8ull));
+  c->st_cap = cap;
+  return REI_OK;
+}
+
+rei_status grow(Ctx* c, uint64_t need_entries);
+
+// The level exchange of north_star / SURVEY 8(e): every rank buckets its locally new
+// CSs (staging list) by hash owner; an all-to-all sends each bucket to its owner; the
+// owner keeps one copy of each CS; the owners' unique lists are all-gathered (owner
+// order) into every rank's arena at `begin` and inserted into its dedup set.  Every
+// rank then holds the same level, byte for byte.  Returns its size.
+rei_status exchange_level(Comm& g, uint64_t begin, const std::vector<LevelCtl>& all, uint64_t* out_count) {
+  const int W = g.world;
+  const size_t nm = g.m.size();
+  rei_status s;
+  Ctx* c0 = g.m[0];
+  const size_t rec = 4ull * (c0->W32 + 2);
+  // 1) bucket the staged entries by owner
+  std::vector<std::vector<uint64_t>> rows(nm, std::vector<uint64_t>(W, 0));
+  for (size_t i = 0; i < nm; ++i) {
+    Ctx* c = g.m[i];
     std::string err;
-    if (!merge_level(c->W32, c->g_cs, c->g_bp, M, c->arena + begin * c->W32, c->bp + begin, &cnt, c->merge,
-                     c->stream, err, &c->launches)) {
+    if (!owner_bucket(c->W32, c->st_cs, c->st_bp, all[g.rank0 + i].count, W, c->xs, c->stream, rows[i].data(), err,
+                      &c->launches)) {
       c->err = err;
       return REI_ECUDA;
     }
-    if (canon != ~0ull && canon != cnt) {
-      g.m[0]->err = c->err = "ranks disagree on the merged level size";
+  }
+  // 2) the G x G count matrix on every rank
+  std::vector<uint64_t> cnt;
+  if ((s = x_gather_u64(g, rows, W, cnt)) != REI_OK) return s;
+  // 3) all-to-all of the buckets
+  std::vector<const uint8_t*> sp(nm);
+  std::vector<uint8_t*> rp(nm);
+  std::vector<uint64_t> mo(nm, 0);
+  for (size_t i = 0; i < nm; ++i) {
+    Ctx* c = g.m[i];
+    const int o = g.rank0 + (int)i;
+    for (int r = 0; r < W; ++r) mo[i] += cnt[(size_t)r * W + o];
+    if (!ensure_recv(c->W32, mo[i], c->xs, c->stream)) { c->err = "exchange receive buffer allocation failed"; return REI_OUT_OF_MEMORY; }
+    sp[i] = static_cast<const uint8_t*>(c->xs.send);
+    rp[i] = static_cast<uint8_t*>(c->xs.recv);
+  }
+  if ((s = x_alltoallv(g, sp, rp, cnt, rec)) != REI_OK) return s;
+  // 4) owner dedup
+  std::vector<std::vector<uint64_t>> un(nm, std::vector<uint64_t>(1, 0));
+  for (size_t i = 0; i < nm; ++i) {
+    Ctx* c = g.m[i];
+    std::string err;
+    if (!owner_dedup(c->W32, mo[i], c->xs, c->stream, &un[i][0], err, &c->launches)) {
+      c->err = err;
       return REI_ECUDA;
     }
-    canon = cnt;
-    // the dedup set must hold every rank's new CSs (present keys are no-ops)
+  }
+  // 5) owner counts, then the unique lists all-gathered in owner order
+  std::vector<uint64_t> u;
+  if ((s = x_gather_u64(g, un, 1, u)) != REI_OK) return s;
+  uint64_t U = 0;
+  for (int r = 0; r < W; ++r) U += u[r];
+  for (size_t i = 0; i < nm; ++i) {
+    Ctx* c = g.m[i];
+    if (!ensure_gather_recs(c->W32, U, c->xs, c->stream)) { c->err = "exchange gather buffer allocation failed"; return REI_OUT_OF_MEMORY; }
+    sp[i] = static_cast<const uint8_t*>(c->xs.uniq);
+    rp[i] = static_cast<uint8_t*>(c->xs.gath);
+  }
+  if ((s = x_allgatherv(g, sp, rp, u, rec)) != REI_OK) return s;
+  // 6) the level into the arena, and into the dedup set (tentative slots re-pointed)
+  for (Ctx* c : g.m) {
+    if (begin + U > c->cap && (s = grow(c, begin + U)) != REI_OK) return s;
+    if (!unpack_records(c->W32, static_cast<const uint32_t*>(c->xs.gath), U, c->arena + begin * c->W32, c->bp + begin,
+                        c->stream, &c->launches)) {
+      c->err = "unpack of the exchanged level failed";
+      return REI_ECUDA;
+    }
     LevelParams p;
     fill_params(c, p);
+    p.stage_cs = c->st_cs;
     EventPair ep;
     c->begin_kernel(REI_K_OTHER, ep);
-    int n = launch_rehash(c->W32, p, begin, cnt, c->stream);
+    int n = launch_rehash(c->W32, p, begin, U, c->stream);
     c->end_kernel(ep, n);
     CUDA_OK(c, cudaGetLastError());
   }
-  *out_count = canon == ~0ull ? 0 : canon;
+  *out_count = U;
   return REI_OK;
 }
 
+// staged = a multi-rank level that is exchanged afterwards: new CSs go to the staging
+// list (and indexed-hash slots are marked tentative) instead of the arena.
 rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, uint64_t nq, uint64_t ns,
-                        const std::vector<Block>& cat, const std::vector<Block>& uni) {
+                        const std::vector<Block>& cat, const std::vector<Block>& uni, bool staged = false) {
   const rei_costs& k = c->costs;
   rei_status s;
   LevelParams p;
   fill_params(c, p);
   p.out_base = begin;
   p.otf = c->otf_level ? 1 : 0;
+  if (staged) {
+    p.arena_out = c->st_cs;
+    p.bp = c->st_bp;
+    p.out_base = 0;
+    p.cap = c->st_cap;
+    p.stage_cs = c->st_cs;
+    p.tent = c->mode == DEDUP_HASHIDX ? 0x80000000u : 0u;
+  }
   if ((s = reset_ctl(c)) != REI_OK) return s;
   // operand blocks -> device (one small H2D per level).  Concatenation blocks are
   // split by orientation (left or right operand sliced): one launch each.
@@ -927,10 +1126,10 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     }
     return REI_OK;
   }
-  if (multi && c0->W32 > 2) {
-    c0->err = "the multi-rank level exchange supports |IC| <= 64";
-    return REI_EINVAL;
-  }
+  // levels with fewer candidates than this run on every rank (no exchange; SURVEY
+  // 8(e) "early levels"), then sorted into a rank-independent order (|IC| <= 64)
+  const uint64_t redundant_below =
+      getenv("REI_REDUNDANT_CAND") ? strtoull(getenv("REI_REDUNDANT_CAND"), nullptr, 10) : 50000000ull;
 
   // ---- level c1: the alphabet symbols (Alg. 1 line 3), identical on every rank
   uint64_t found_seed = ~0ull;
@@ -1004,12 +1203,18 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     // than ~4x the previous level's new CSs; an overflow still triggers a retry).  In
     // multi-rank mode a rank also stages its own list there, hence the factor 2.
     const uint64_t prev = c0->stats.empty() ? 0 : c0->stats.back().unique;
-    const uint64_t expect = std::min<uint64_t>(nq + ns + ncat + nuni, (multi ? 8 : 4) * prev + 1024);
+    const uint64_t expect = std::min<uint64_t>(nq + ns + ncat + nuni, 4 * prev + 1024);
+    // multi-rank: a small level runs whole on every rank; a large one is split by
+    // rei_partition and exchanged by hash owner
+    const uint64_t level_cand = nq + ns + ncat + nuni;
+    const bool redundant = multi && !otf && c0->W32 <= 2 && level_cand < redundant_below;
+    const bool staged = multi && !otf && !redundant;
     for (Ctx* c : g.m) {
       if (otf) break;
       if (c->arena_used + expect > c->cap || c->slabs_used + expect / 32 + 2 > c->slab_cap) {
         if ((s = grow(c, c->arena_used + expect)) != REI_OK && s != REI_OUT_OF_MEMORY) return s;
       }
+      if (staged && (s = ensure_stage(c, expect)) != REI_OK) return s;
     }
     lv.begin = c0->arena_used;
     lv.slab = c0->slabs_used;
@@ -1019,7 +1224,8 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     double level_ms = 0;
     for (int attempt = 0;; ++attempt) {
       for (size_t i = 0; i < g.m.size(); ++i)
-        if ((s = launch_level(g.m[i], g.rank0 + (int)i, g.world, cost, lv.begin, nq, ns, cat, uni)) != REI_OK)
+        if ((s = launch_level(g.m[i], redundant ? 0 : g.rank0 + (int)i, redundant ? 1 : g.world, cost, lv.begin, nq,
+                              ns, cat, uni, staged)) != REI_OK)
           return s;
       for (Ctx* c : g.m) {
         if ((s = read_ctl(c)) != REI_OK) return s;
@@ -1029,12 +1235,32 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
       }
       if ((s = gather_ctl(g, all)) != REI_OK) return s;
       bool overflow = false;
-      uint64_t need = 0;
+      uint64_t need = 0, need_stage = 0;
       for (auto& l : all) {
         overflow |= l.overflow != 0;
         need = std::max<uint64_t>(need, lv.begin + l.count + 1);
+        need_stage = std::max<uint64_t>(need_stage, l.count + 1);
       }
       if (!overflow) break;
+      if (staged) {
+        // the staging list (or the dedup set) overflowed: a larger list, a clean dedup
+        // set (drops this attempt's tentative inserts), and the arena if it is short
+        bool grew = false;
+        for (Ctx* c : g.m) {
+          if ((s = ensure_stage(c, std::max<uint64_t>(2 * c->st_cap, need_stage))) != REI_OK) return s;
+          if (lv.begin + need_stage > c->cap || attempt >= 1) {
+            if ((s = grow(c, std::max<uint64_t>(lv.begin + need_stage, c->cap + 1))) != REI_OK) return s;
+            grew = true;
+          } else if ((s = rebuild_dedup(c, c->arena_used)) != REI_OK) {
+            return s;
+          }
+        }
+        if (attempt > 8 && !grew) {
+          c0->err = "multi-rank level keeps overflowing";
+          return REI_OUT_OF_MEMORY;
+        }
+        continue;
+      }
       // capacity exceeded: grow the cache / dedup set and redo the level; when the
       // budget is exhausted, switch to OnTheFly mode and re-check the level
       bool to_otf = false;
@@ -1072,8 +1298,22 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     const bool found = found_rank != ~0ull;
     const bool complete = !found || (c0->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
     uint64_t size = otf_now ? 0 : all[g.rank0].count;
-    if (multi && complete && !otf_now) {
+    if (staged && complete && !otf_now) {
       if ((s = exchange_level(g, lv.begin, all, &size)) != REI_OK) return s;
+    }
+    if (redundant && complete && !otf_now) {
+      for (Ctx* c : g.m) {
+        if (c->h_ctl->count != size) {
+          c->err = "ranks disagree on the size of a redundantly computed level";
+          return REI_ECUDA;
+        }
+        std::string err;
+        if (!canon_sort_level(c->W32, (uint32_t)c->tab.n, c->arena + lv.begin * c->W32, c->bp + lv.begin, size,
+                              c->merge, c->stream, err, &c->launches)) {
+          c->err = err;
+          return REI_ECUDA;
+        }
+      }
     }
     lv.size = size;
     st.unique = size;
@@ -1104,7 +1344,7 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
       c->result.candidates = cand;
       c->result.last_complete_cost = (uint32_t)cost;
       if (otf_now) continue;  // nothing cached at this level
-      if (c->sort_levels && lv.size >= (1u << 14)) {  // bitmap mode: order by bitmap position (exchange.cu)
+      if (c->sort_levels && lv.size >= (1u << 14) && !redundant) {  // bitmap mode: order by bitmap position
         std::string err;
         if (!sort_level((uint32_t)c->tab.n, c->arena + lv.begin, c->bp + lv.begin, lv.size, c->merge, c->stream,
                         err, &c->launches)) {
@@ -1636,6 +1876,7 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
   g.world = c->world > 1 ? c->world : 1;
   g.rank0 = c->world > 1 ? c->rank : 0;
   g.nccl = c->nccl;
+  g.host = c->world > 1 && c->host_xport;
   if (c->sharded && c->world > 1) return solve_sharded(g, max_cost);
   return solve_group(g, max_cost);
 }
@@ -1726,12 +1967,16 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       c->world = opts->world_size;
       c->rank = opts->rank;
     } else if (opts->world_size > 1) {
-      if (!opts->nccl_unique_id || opts->rank < 0 || opts->rank >= opts->world_size) {
-        g_init_error = "multi-GPU context needs rank in [0, world_size) and an ncclUniqueId";
+      if ((!opts->nccl_unique_id && !opts->allgather) || opts->rank < 0 || opts->rank >= opts->world_size ||
+          opts->world_size > 64) {
+        g_init_error = "multi-GPU context needs rank in [0, world_size <= 64) and an ncclUniqueId or an "
+                       "allgather callback";
         return REI_EINVAL;
       }
       c->world = opts->world_size;
       c->rank = opts->rank;
+      // no NCCL id: the level exchange goes through the host all-gather callback
+      c->host_xport = opts->nccl_unique_id == nullptr;
     }
   }
   if (opts && opts->device >= 0) {
@@ -1766,7 +2011,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   phase("aux streams + small buffers");
   c->ctl = c->ctl_base;
   cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
-  if (c->world > 1 && !c->sharded) {  // one process per GPU: the level exchange runs over NCCL (collective)
+  if (c->world > 1 && !c->sharded && !c->host_xport) {  // one process per GPU: the exchange runs over NCCL
     ncclUniqueId id;
     memcpy(&id, opts->nccl_unique_id, sizeof(id));
     ncclComm_t comm;
@@ -1775,7 +2020,8 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       return REI_ENCCL;
     }
     c->nccl = comm;
-    if (c->dmalloc(&c->d_ctl_all, sizeof(LevelCtl) * c->world) != cudaSuccess)
+    if (c->dmalloc(&c->d_ctl_all, sizeof(LevelCtl) * c->world) != cudaSuccess ||
+        c->dmalloc(&c->d_small, 64 * 8) != cudaSuccess || c->dmalloc(&c->d_small_all, 64 * 8 * c->world) != cudaSuccess)
       return fail("device allocation failed (control lines)");
   }
   if (c->P.empty() && c->N.empty()) {
@@ -2104,6 +2350,39 @@ rei_status rei_solve_batch(void* const* ctxs, size_t n, uint32_t max_cost, int t
   worker();
   for (auto& th : pool) th.join();
   return REI_OK;
+}
+
+int rei_cs_owner(const uint32_t* cs, uint32_t cs_words, int world) {
+  if (world <= 1 || !cs) return 0;
+  switch (cs_words) {
+#define REI_OWNER_CASE(W)                                          \
+  case W: {                                                        \
+    uint32_t x[W];                                                 \
+    for (int q = 0; q < W; ++q) x[q] = cs[q];                      \
+    return (int)rei::owner_of_hash(rei::hash_cs<W>(x), (uint32_t)world); \
+  }
+    REI_OWNER_CASE(1)
+    REI_OWNER_CASE(2)
+    REI_OWNER_CASE(4)
+    REI_OWNER_CASE(8)
+    REI_OWNER_CASE(16)
+#undef REI_OWNER_CASE
+    default:
+      return -1;
+  }
+}
+
+void rei_exchange_offsets(int world, const uint64_t* counts, int rank, uint64_t* send_off, uint64_t* recv_off) {
+  for (int o = 0; o < world; ++o) {
+    uint64_t x = 0;
+    for (int q = 0; q < o; ++q) x += counts[(size_t)rank * world + q];
+    if (send_off) send_off[o] = x;
+  }
+  for (int r = 0; r < world; ++r) {
+    uint64_t x = 0;
+    for (int q = 0; q < r; ++q) x += counts[(size_t)q * world + rank];
+    if (recv_off) recv_off[r] = x;
+  }
 }
 
 void rei_partition(uint64_t total, int G, int g, uint64_t* begin, uint64_t* end) {

@@ -100,8 +100,32 @@ struct LevelParams {
   uint32_t pad_s;
   const Peer* peers;          // [shards], device memory of this rank
   uint64_t rank_base;         // unary kernels: rank of their first candidate
+  const uint32_t* stage_cs;   // multi-rank levels: the staging list (== arena_out while the
+                              // level runs) that tentative indexed-hash slots point into
+  uint32_t tent;              // kTent in multi-rank levels with the indexed hash set, else 0
+  uint32_t pad_t;
   uint32_t pos[kMaxW32];
   uint32_t neg[kMaxW32];
 };
+
+#ifdef __CUDACC__
+// 64-bit hash of a CS (W 32-bit words): slot bits of the dedup sets, and the owner
+// rank (bits 40.., independent of the slot bits) of the multi-GPU exchange and of the
+// sharded cache.  Host and device share it (rei_cs_owner).
+template <int W>
+__host__ __device__ __forceinline__ unsigned long long hash_cs(const uint32_t (&cs)[W]) {
+  unsigned long long h = 0x9E3779B97F4A7C15ull;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    h = (h ^ cs[q]) * 0xBF58476D1CE4E5B9ull;
+    h ^= h >> 31;
+  }
+  h *= 0x94D049BB133111EBull;
+  return h ^ (h >> 29);
+}
+__host__ __device__ __forceinline__ uint32_t owner_of_hash(unsigned long long h, uint32_t world) {
+  return (uint32_t)(h >> 40) % world;
+}
+#endif
 
 }  // namespace rei

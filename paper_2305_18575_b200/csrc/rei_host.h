@@ -50,6 +50,28 @@ void free_merge_scratch(MergeScratch& s);
 // Reorder a finished one-word (bitmap-mode) level by bitmap position, in place.
 bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, MergeScratch& s, cudaStream_t st,
                 std::string& err, uint64_t* launches);
+// Hash-owner exchange of a multi-rank level (exchange.cu).  Records are
+// (CS words, back-pointer as 2 words), 4 * (W32 + 2) bytes each.
+struct XScratch {
+  void *owner = nullptr, *send = nullptr, *recv = nullptr, *uniq = nullptr, *gath = nullptr, *table = nullptr,
+       *ctr = nullptr;
+  size_t owner_cap = 0, send_cap = 0, recv_cap = 0, uniq_cap = 0, gath_cap = 0, table_cap = 0, ctr_cap = 0;
+};
+// Bucket the m staged entries by hash owner into x.send (owner-contiguous records);
+// counts[o] (host) = records owned by rank o.
+bool owner_bucket(int W32, const uint32_t* cs, const unsigned long long* bp, uint64_t m, int world, XScratch& x,
+                  cudaStream_t st, uint64_t* counts, std::string& err, uint64_t* launches);
+bool ensure_recv(int W32, uint64_t m, XScratch& x, cudaStream_t st);
+// Dedup the m records of x.recv into x.uniq (first insert of each CS wins); *out_count.
+bool owner_dedup(int W32, uint64_t m, XScratch& x, cudaStream_t st, uint64_t* out_count, std::string& err,
+                 uint64_t* launches);
+bool ensure_gather_recs(int W32, uint64_t m, XScratch& x, cudaStream_t st);
+bool unpack_records(int W32, const uint32_t* rec, uint64_t m, uint32_t* cs, unsigned long long* bp, cudaStream_t st,
+                    uint64_t* launches);
+// Sort a level computed redundantly on every rank into a rank-independent order (by CS).
+bool canon_sort_level(int W32, uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, MergeScratch& s,
+                      cudaStream_t st, std::string& err, uint64_t* launches);
+void free_xscratch(XScratch& x);
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                uint64_t count, cudaStream_t st);
 

@@ -146,6 +146,11 @@ def load_library():
     lib.rei_cs_ops.argtypes = [vp, c.c_int, c.POINTER(c.c_uint32), c.POINTER(c.c_uint32),
                                c.POINTER(c.c_uint32), c.c_size_t]
     lib.rei_partition.argtypes = [c.c_uint64, c.c_int, c.c_int, c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)]
+    lib.rei_cs_owner.restype = c.c_int
+    lib.rei_cs_owner.argtypes = [c.POINTER(c.c_uint32), c.c_uint32, c.c_int]
+    lib.rei_exchange_offsets.restype = None
+    lib.rei_exchange_offsets.argtypes = [c.c_int, c.POINTER(c.c_uint64), c.c_int, c.POINTER(c.c_uint64),
+                                         c.POINTER(c.c_uint64)]
     lib.rei_nccl_unique_id.restype = c.c_int
     lib.rei_nccl_unique_id.argtypes = [c.c_void_p, c.c_size_t]
     lib.rei_solve_batch.restype = c.c_int
@@ -213,9 +218,12 @@ class Solver:
                  complete_final_level: bool = False, world_size: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, max_entries: int = 0, onthefly: bool = True,
                  sharded_cache: bool = False, allgather=None):
-        """sharded_cache: capacity mode (include/rei.h REI_FLAG_SHARDED_CACHE).  With
-        world_size > 1 (one process per rank) `allgather` is a Python all-gather
-        (bytes -> list of bytes); default: torch_allgather() over torch.distributed."""
+        """world_size > 1 (one process per rank, rei_solve collective): the level
+        exchange runs over NCCL with `nccl_id` (rank 0's nccl_unique_id()), or, with
+        `allgather` and no nccl_id, through that host all-gather (bytes -> list of
+        bytes in rank order, e.g. torch_allgather() over gloo).
+        sharded_cache: capacity mode (include/rei.h REI_FLAG_SHARDED_CACHE); `allgather`
+        defaults to torch_allgather() there."""
         lib = load_library()
         self._lib = lib
         self._h = ctypes.c_void_p()
@@ -225,9 +233,14 @@ class Solver:
         if world_size > 1 and sharded_cache:
             self._allgather = c_allgather(allgather or torch_allgather())
             opts.allgather = self._allgather
+        elif world_size > 1 and allgather is not None and nccl_id is None:
+            # host-staged level exchange through the caller's all-gather (e.g. gloo)
+            self._allgather = c_allgather(allgather)
+            opts.allgather = self._allgather
         elif world_size > 1:
             if nccl_id is None or len(nccl_id) < 128:
-                raise ValueError("world_size > 1 needs the 128-byte nccl_id from rank 0")
+                raise ValueError("world_size > 1 needs the 128-byte nccl_id from rank 0 "
+                                 "(or an allgather callable for the host-staged exchange)")
             _use_torch_nccl()
             self._nccl_id = ctypes.create_string_buffer(bytes(nccl_id), 128)
             opts.nccl_unique_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
@@ -404,6 +417,24 @@ def partition(total: int, G: int, g: int) -> Tuple[int, int]:
     b, e = ctypes.c_uint64(), ctypes.c_uint64()
     lib.rei_partition(total, G, g, ctypes.byref(b), ctypes.byref(e))
     return b.value, e.value
+
+
+def cs_owner(cs: int, cs_words: int, world: int) -> int:
+    """rei_cs_owner: the hash owner of a CS among `world` ranks (host logic)."""
+    lib = load_library()
+    arr = (ctypes.c_uint32 * cs_words)(*[(cs >> (32 * q)) & 0xFFFFFFFF for q in range(cs_words)])
+    return lib.rei_cs_owner(arr, cs_words, world)
+
+
+def exchange_offsets(world: int, counts: Sequence[int], rank: int) -> Tuple[List[int], List[int]]:
+    """rei_exchange_offsets: (send offsets by owner, receive offsets by source) of the
+    level all-to-all for `rank`, from the world x world count matrix (row = source)."""
+    lib = load_library()
+    c = (ctypes.c_uint64 * (world * world))(*counts)
+    so = (ctypes.c_uint64 * world)()
+    ro = (ctypes.c_uint64 * world)()
+    lib.rei_exchange_offsets(world, c, rank, so, ro)
+    return list(so), list(ro)
 
 
 def _use_torch_nccl():

@@ -28,6 +28,11 @@ SPECS = {
     "intro": (specgen.INTRO, 20),
     # BASELINE configs[1]: Type 1, binary, le = 6, p = n = 10, seed 0
     "c2_t1_s0": (specgen.gen_type1("01", 6, 10, 10, 0), 40),
+    # BASELINE configs[2]: binary, |IC| = 115 (two-u64 CS), planted target, unit and the
+    # non-uniform cost function (20,20,20,5,30) (the paper's AlphaRegex-style costs)
+    "c3_planted_s1": (specgen.gen_planted("01", "(0+1)*1(0+1)(0+1)(0+1)", 10, 10, 6, 10, 1), 40),
+    "c3_planted_s1_nu": (specgen.gen_planted("01", "(0+1)*1(0+1)(0+1)(0+1)", 10, 10, 6, 10, 1,
+                                             costs=(20, 20, 20, 5, 30)), 800),
     # BASELINE configs[3]: 4 symbols, planted target (DESIGN.md input recipe), |IC| = 148
     "c4_planted_s0": (specgen.gen_planted("abcd", "(a+b+c)*d(a+c)(b+d)", 10, 10, 4, 8, 0), 40),
 }

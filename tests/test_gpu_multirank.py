@@ -1,9 +1,12 @@
 """Sharded level with virtual ranks on one GPU (``-m gpu``).
 
 G contexts act as ranks 0..G-1 of one search: each enumerates its share of every
-level, the new-CS lists are all-gathered (device copies instead of NCCL) and
-merged canonically.  Checked against the oracle: same c*, the same set of CSs at
-every level, and every rank holding a byte-identical cache (same order)."""
+level and stages the CSs new to it; the staged CSs go to their hash owners
+(all-to-all), the owners deduplicate, and the unique lists are all-gathered (device
+copies instead of NCCL).  Small levels run whole on every rank and are sorted into a
+canonical order (REI_REDUNDANT_CAND; 0 = exchange every level).  Checked against
+the oracle: same c*, the same set of CSs at every level, and every rank holding a
+byte-identical cache (same order)."""
 import json
 import os
 
@@ -36,9 +39,29 @@ CASES = [(specgen.C1_TOY, 12), (specgen.E1, 12), (specgen.TABLE1_ROW1, 15),
          (specgen.C1_TOY.with_costs((2, 1, 3, 1, 1)), 20)]
 
 
+@pytest.fixture(params=["0", "2000"], ids=["exchange-all", "redundant-small"])
+def redundant(request, monkeypatch):
+    monkeypatch.setenv("REI_REDUNDANT_CAND", request.param)
+    return request.param
+
+
+WIDE = [(specgen.gen_planted("01", "(0+1)*0(0+1)(0+1)", 10, 10, 4, 8, 1), 11),       # |IC| 69: W32 = 4
+        (specgen.gen_planted("01", "1(0+11)*0?", 10, 10, 6, 12, 0), 8),               # W32 = 8
+        (specgen.gen_planted("abcd", "(a+b)*c(a+d)*", 10, 10, 6, 14, 1), 8)]          # W32 = 16
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("sp,K", WIDE, ids=["w4", "w8", "w16"])
+def test_virtual_ranks_wide_match_oracle(sp, K, G, monkeypatch):
+    # indexed hash set: tentative slots of the staged lists are re-pointed after the
+    # exchange; every level is exchanged (no redundant mode above 64 bits)
+    monkeypatch.setenv("REI_REDUNDANT_CAND", "0")
+    test_virtual_ranks_match_oracle(sp, K, G, None)
+
+
 @pytest.mark.parametrize("G", [2, 3, 4])
 @pytest.mark.parametrize("sp,K", CASES, ids=[c[0].name or "rand" for c in CASES])
-def test_virtual_ranks_match_oracle(sp, K, G):
+def test_virtual_ranks_match_oracle(sp, K, G, redundant):
     from paper_2305_18575_b200 import solve_group
     o = oracle.Oracle.from_spec(sp)
     ro = o.solve(K, complete_final_level=True)
@@ -69,16 +92,21 @@ def test_virtual_ranks_early_exit(G):
     assert rg.cand_complete == ro.cand_complete
 
 
-def test_virtual_ranks_table1_row1_full():
-    # the bench workload sharded over 2 virtual ranks: c* = 28 and the golden counts
+@pytest.mark.parametrize("G", [2, 4])
+def test_virtual_ranks_table1_row1_full(G):
+    # the bench workload sharded over virtual ranks (default threshold: levels >= 20
+    # are exchanged): c* = 28 and the oracle golden's counts on every rank
     from paper_2305_18575_b200 import solve_group
     sp = specgen.TABLE1_ROW1
-    rg = solve_group(group(sp, 2), 40)
+    members = group(sp, G)
+    rg = solve_group(members, 40)
     assert rg.status == "found" and rg.cost == 28
     assert precise(rg.regex, sp.P, sp.N)
-    path = os.path.join(GOLDEN, "table1_row1_oracle.json")
-    if os.path.exists(path):
-        want = {l["cost"]: l["unique"] for l in json.load(open(path))["levels"]}
-        for l in rg.levels:
+    want = {l["cost"]: l["unique"] for l in json.load(open(os.path.join(GOLDEN, "table1_row1_oracle.json")))["levels"]}
+    for m in members:
+        for l in m.level_stats():
             if l.cost < 28:
                 assert l.unique == want[l.cost], l.cost
+    for c in (20, 27):  # deep exchanged levels are byte-identical across ranks
+        first = members[0].level_cs(c)
+        assert all(m.level_cs(c) == first for m in members[1:])

@@ -2,9 +2,11 @@
 
 * every rank's share of a level's work lists (rei_partition, the C ABI's pure host
   function) is disjoint and the shares cover the list exactly;
-* the level exchange protocol: ranks all-gather their new-CS lists in rank order
-  and keep first occurrences -- every rank derives the same canonical list, equal
-  to the union of the lists;
+* the level exchange protocol driven by the library's host functions (rei_cs_owner,
+  rei_exchange_offsets): bucket by hash owner, all-to-all, owner dedup, all-gather
+  of the owners' lists -- every rank derives the same level, the union of the
+  staged lists (the device side of the same exchange runs in
+  tests/test_gpu_multiproc.py);
 * bench.py's cross-rank reduction: time = max over ranks, work = sum;
 * the sharded cache's host transport (REI_FLAG_SHARDED_CACHE): the C all-gather
   callback the binding builds on torch.distributed returns every rank's bytes in
@@ -48,17 +50,48 @@ def _worker(rank, world, port, q):
             assert spans[0][0] == 0 and spans[-1][1] == total
             for (b0, e0), (b1, e1) in zip(spans, spans[1:]):
                 assert e0 == b1 and b0 <= e0
-        # 2) canonical merge of per-rank lists (first occurrence, rank order)
-        rng = random.Random(100 + rank)
-        mine = [rng.randrange(50) for _ in range(40)]
-        mine = list(dict.fromkeys(mine))  # a rank's own list has no duplicates
-        lists = [None] * world
-        dist.all_gather_object(lists, mine)
-        merged = list(dict.fromkeys(x for l in lists for x in l))
-        views = [None] * world
-        dist.all_gather_object(views, merged)
-        assert all(v == views[0] for v in views)
-        assert set(merged) == set().union(*map(set, lists))
+        # 2) the level exchange protocol with the library's host functions: a rank's
+        #    staged CSs are bucketed by rei_cs_owner, sent to their owners at the
+        #    rei_exchange_offsets positions (all-to-all over gloo), deduplicated by the
+        #    owner, and the owners' lists all-gathered in owner order -- every rank gets
+        #    the same level, the union of the staged lists without duplicates
+        from paper_2305_18575_b200 import cs_owner, exchange_offsets
+        for words in (1, 2, 4, 16):
+            rng = random.Random(100 + rank + words)
+            pool = [rng.getrandbits(32 * words) for _ in range(60)]
+            pool_all = [None] * world
+            dist.all_gather_object(pool_all, pool)
+            common = pool_all[0][:20]  # CSs several ranks find (cross-rank duplicates)
+            mine = list(dict.fromkeys(common + pool[20:]))
+            owners = [cs_owner(x, words, world) for x in mine]
+            assert all(0 <= o < world for o in owners)
+            buckets = [[x for x, o in zip(mine, owners) if o == d] for d in range(world)]
+            row = [len(b) for b in buckets]
+            rows = [None] * world
+            dist.all_gather_object(rows, row)
+            counts = [c for r in rows for c in r]
+            send_off, recv_off = exchange_offsets(world, counts, rank)
+            flat = [x for b in buckets for x in b]
+            assert all(flat[send_off[d]:send_off[d] + row[d]] == buckets[d] for d in range(world))
+            sent = [None] * world
+            dist.all_gather_object(sent, flat)  # gloo stands in for the all-to-all
+            recv = []
+            for src in range(world):
+                so, _ = exchange_offsets(world, counts, src)
+                chunk = sent[src][so[rank]:so[rank] + counts[src * world + rank]]
+                assert len(recv) == recv_off[src]
+                recv += chunk
+            assert all(cs_owner(x, words, world) == rank for x in recv)
+            uniq = list(dict.fromkeys(recv))
+            lists = [None] * world
+            dist.all_gather_object(lists, uniq)
+            level = [x for l in lists for x in l]
+            views = [None] * world
+            dist.all_gather_object(views, level)
+            assert all(v == views[0] for v in views)
+            staged = [None] * world
+            dist.all_gather_object(staged, mine)
+            assert sorted(level) == sorted(set().union(*map(set, staged)))
         # 3) bench.py reduction
         import bench
         t, c = bench.reduce_over_ranks(10.0 + rank, 1000 * (rank + 1), torch.device("cpu"), world)
