@@ -48,6 +48,16 @@ WORKLOADS = {
                  "(|IC|=58, two-word CS, 64-bit-key hash set)"),
     "c2-t1-s3": (specgen.gen_type1("01", 6, 10, 10, 3), 40,
                  "BASELINE configs[1]: Type 1 binary, le=6, p=n=10, seed 3 (|IC|=55)"),
+    "c3-planted-s1": (specgen.gen_planted("01", "(0+1)*1(0+1)(0+1)(0+1)", 10, 10, 6, 10, 1), 40,
+                      "BASELINE configs[2]: planted binary target (DESIGN.md recipe), |IC|=115 (two-u64 CS, "
+                      "indexed hash set), unit costs (c*=18)"),
+    "c3-planted-s1-nu": (specgen.gen_planted("01", "(0+1)*1(0+1)(0+1)(0+1)", 10, 10, 6, 10, 1,
+                                             costs=(20, 20, 20, 5, 30)), 800,
+                         "BASELINE configs[2]: the same spec, non-uniform costs (20,20,20,5,30) (P:1356 style), "
+                         "c*=325, 1.2e9 candidates"),
+    "c4-planted-s0": (specgen.gen_planted("abcd", "(a+b+c)*d(a+c)(b+d)", 10, 10, 4, 8, 0), 40,
+                      "BASELINE configs[3]: planted 4-symbol target, |IC|=148 (256-bit CS), unit costs (c*=16), "
+                      "5e8 candidates"),
     "c2-t2-s4": (specgen.gen_type2("01", 6, 10, 10, 4), 40,
                  "BASELINE configs[1]: Type 2 (P:1244-1253) binary, le=6, p=n=10, seed 4 "
                  "(|IC|=48, c*=25, ~2.7e10 candidates, 1.5e9 cached CSs)"),
@@ -59,8 +69,12 @@ PAPER = {
     "table1-row8": {"reps": 23349552935, "gpu_s": 4.9096, "cpu_s": 4519.9456,
                     "hw": "Colab A100-SXM4-40GB (P:1147-1153)"},
 }
-ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8, "c2-t1-s0": 16, "c2-t1-s3": 16, "c2-t2-s4": 16}   # cpu_baseline sample
-REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8, "c2-t1-s0": 14, "c2-t1-s3": 14, "c2-t2-s4": 14}  # --impl reference step
+ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8, "c2-t1-s0": 16, "c2-t1-s3": 16,
+                      "c2-t2-s4": 16, "c3-planted-s1": 13, "c3-planted-s1-nu": 245, "c4-planted-s0": 11}
+# cpu_baseline sample
+REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8, "c2-t1-s0": 14, "c2-t1-s3": 14,
+                       "c2-t2-s4": 14, "c3-planted-s1": 12, "c3-planted-s1-nu": 230, "c4-planted-s0": 10}
+# --impl reference step
 
 METRIC = "candidate REs/sec"
 UNIT = "cand/s"

@@ -362,19 +362,28 @@ class Solver:
         self._lib.rei_masks(self._h, p, q)
         return _words_to_int(p, W), _words_to_int(q, W)
 
-    def level_cs(self, cost: int) -> List[int]:
+    def level_cs_array(self, cost: int):
+        """The CSs of level `cost` as a numpy uint32 array of shape (m, cs_words)."""
+        import numpy as np
         W = self.cs_words
         cnt = ctypes.c_size_t()
         self._lib.rei_level_cs(self._h, cost, None, 0, ctypes.byref(cnt))
         m = cnt.value
+        arr = np.zeros(max(1, m) * W, dtype=np.uint32)
+        if m:
+            st = self._lib.rei_level_cs(self._h, cost, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+                                        m, ctypes.byref(cnt))
+            if st != REI_OK:
+                raise ReiError(st, self._err())
+        return arr[:m * W].reshape(m, W)
+
+    def level_cs(self, cost: int) -> List[int]:
+        W = self.cs_words
+        arr = self.level_cs_array(cost)
+        m = arr.shape[0]
         if m == 0:
             return []
-        import numpy as np
-        arr = np.zeros(m * W, dtype=np.uint32)
-        st = self._lib.rei_level_cs(self._h, cost, arr.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
-                                    m, ctypes.byref(cnt))
-        if st != REI_OK:
-            raise ReiError(st, self._err())
+        arr = arr.reshape(-1)
         if W == 1:
             return [int(x) for x in arr]
         arr = arr.reshape(m, W).astype(object)

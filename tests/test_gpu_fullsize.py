@@ -1,29 +1,36 @@
-"""Full-size BASELINE configs, launched as bench.py launches them (``-m gpu``).
+"""Full-size BASELINE configs, launched as bench.py launches them (``-m gpu``),
+against oracle-written golden files (``tests/golden/<name>_oracle.json``, written by
+``scripts/make_golden.py``, which calls only ``oracle/``).
 
-The oracle cannot finish these, so parity is checked by
-properties that hold at any size and by the oracle on what it can compute:
-* the returned regex is precise under Python's ``re`` and costs exactly c*;
-* the oracle's per-level unique and candidate counts for the levels it finishes;
-* sampled cache entries of the deepest levels: the regex reconstructed from each
-  entry's back-pointer denotes exactly the stored CS on IC (checked
-  with ``re``) and costs exactly its level;
-* no cached CS of a level below c* is precise (the search would have stopped).
-C5 (Table 1 row 1) is compared against the oracle's golden file in
-test_gpu_parity.py.
+For every workload: the same minimal cost c* as the oracle; identical per-level
+unique counts and per-constructor candidate counts (reading A9) for every level
+below c* (the golden's search stops at the first precise candidate, like the
+bench); the returned regex is precise under Python's ``re`` and costs exactly c*;
+sampled cache entries of the deepest levels reconstruct to regexes
+that denote exactly the stored CS on IC and cost exactly their level; no cached CS
+below c* is precise.  A missing golden FAILS the test.
+C5 (Table 1 row 1) is compared against its golden in test_gpu_parity.py.
 """
 import json
 import os
 import random
 
+import numpy as np
 import pytest
 
 import bench
-import oracle
-import specgen
 from regex_tools import cost as re_cost, language_on, parse, precise
 
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+FULL = [  # (bench workload, golden file stem)
+    ("c2-t1-s0", "c2_t1_s0"),                  # configs[1]: |IC| 58, 64-bit-key hash set
+    ("c3-planted-s1", "c3_planted_s1"),        # configs[2]: |IC| 115, indexed hash set, unit costs
+    ("c3-planted-s1-nu", "c3_planted_s1_nu"),  # configs[2]: non-uniform costs (20,20,20,5,30)
+    ("c4-planted-s0", "c4_planted_s0"),        # configs[3]: |IC| 148, 4 symbols
+    ("table1-row8", "table1_row8"),            # Table 1 row 8, costs (10,10,10,1,10)
+]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -35,67 +42,56 @@ def _need_gpu():
     build.build()
 
 
-def check_full(name, oracle_levels):
+def load_golden(stem, spec):
+    path = os.path.join(GOLDEN, f"{stem}_oracle.json")
+    assert os.path.exists(path), f"missing oracle golden {path}: python scripts/make_golden.py {stem}"
+    gold = json.load(open(path))
+    g = gold["spec"]
+    assert (g["alphabet"], tuple(g["P"]), tuple(g["N"]), tuple(g["costs"])) == \
+        (spec.alphabet, tuple(spec.P), tuple(spec.N), tuple(spec.costs)), "golden is for another spec"
+    assert gold["status"] == "found"
+    return gold
+
+
+@pytest.mark.parametrize("workload,stem", FULL, ids=[f[0] for f in FULL])
+def test_full_size_vs_oracle_golden(workload, stem):
     from paper_2305_18575_b200 import Solver
-    spec, max_cost, _ = bench.WORKLOADS[name]
+    spec, max_cost, _ = bench.WORKLOADS[workload]
+    gold = load_golden(stem, spec)
+    cstar = gold["cstar"]
     g = Solver.from_spec(spec, device=0)
     r = g.solve(max_cost)
     assert r.status == "found"
+    assert r.cost == cstar, (r.cost, cstar)
     assert precise(r.regex, spec.P, spec.N), r.regex
-    assert re_cost(parse(r.regex), spec.costs) == r.cost
-    # oracle on the levels it can finish in seconds
-    ro = oracle.Oracle.from_spec(spec).solve(oracle_levels)
-    got = {l.cost: (l.unique, l.cand) for l in r.levels}
-    for l in ro.levels:
-        if l.complete and l.cost in got:
-            assert got[l.cost] == (l.unique, l.cand), l.cost
+    assert re_cost(parse(r.regex), spec.costs) == cstar
+    want = {l["cost"]: l for l in gold["levels"] if l["cost"] < cstar}
+    got = {l.cost: l for l in r.levels if l.cost < cstar}
+    assert sorted(got) == sorted(want)
+    for c, l in got.items():
+        w = want[c]
+        assert l.complete and w["complete"], c
+        assert (l.unique, l.cand_q, l.cand_s, l.cand_c, l.cand_u) == \
+            (w["unique"], w["cand_q"], w["cand_s"], w["cand_c"], w["cand_u"]), c
     # sampled reconstruction audit of the deepest complete levels
     ic = g.ic()
     idx = {w: i for i, w in enumerate(ic)}
     pm, nm = g.masks()
     rng = random.Random(5)
-    deep = [l.cost for l in r.levels if l.complete and l.unique][-3:]
+    deep = [c for c in sorted(got) if got[c].unique][-3:]
+    W = r.cs_words
+    pw = np.array([(pm >> (32 * q)) & 0xFFFFFFFF for q in range(W)], dtype=np.uint32)
+    nw = np.array([(nm >> (32 * q)) & 0xFFFFFFFF for q in range(W)], dtype=np.uint32)
     for c in deep:
-        cs = g.level_cs(c)
-        for i in rng.sample(range(len(cs)), min(40, len(cs))):
+        arr = g.level_cs_array(c)
+        assert arr.shape[0] == got[c].unique
+        for i in rng.sample(range(arr.shape[0]), min(30, arr.shape[0])):
             rx = g.entry_regex(c, i)
-            assert sum(1 << idx[w] for w in language_on(rx, ic)) == cs[i], (c, i, rx)
+            cs_i = sum(int(arr[i, q]) << (32 * q) for q in range(W))
+            assert sum(1 << idx[w] for w in language_on(rx, ic)) == cs_i, (c, i, rx)
             assert re_cost(parse(rx), spec.costs) == c
         # P12 / minimality: nothing cached below c* is precise
-        assert not any((x & pm) == pm and not (x & nm) for x in cs)
-    return r
-
-
-def test_c2_type1_seed0_full():
-    # BASELINE configs[1]: |IC| = 58, two-word CSs, 64-bit-key hash set, c* = 23
-    r = check_full("c2-t1-s0", 14)
-    assert r.cost == 23 and r.cs_words == 2
-
-
-def test_table1_row8_full():
-    # Table 1 row 8: the row-1 spec with costs (10,10,10,1,10); c* = 208
-    r = check_full("table1-row8", 130)
-    assert r.cost == 208
-    path = os.path.join(GOLDEN, "table1_row8_oracle.json")
-    if os.path.exists(path):
-        gold = json.load(open(path))
-        assert gold["cstar"] == r.cost
-        want = {l["cost"]: l["unique"] for l in gold["levels"]}
-        for l in r.levels:
-            if l.complete:
-                assert l.unique == want[l.cost], l.cost
-
-
-@pytest.mark.parametrize("alpha,tgt,lo,hi,seed", [
-    ("01", "(0+1)*0(0+1)(0+1)", 6, 12, 0),       # configs[2]: W32 = 8
-    ("abcd", "(ab+c)*d(a+b)?", 6, 14, 1),        # configs[3]: W32 = 16
-])
-def test_planted_wide_full(alpha, tgt, lo, hi, seed):
-    from paper_2305_18575_b200 import Solver
-    sp = specgen.gen_planted(alpha, tgt, 10, 10, lo, hi, seed)
-    g = Solver.from_spec(sp, device=0)
-    r = g.solve(30)
-    assert r.status == "found"
-    assert precise(r.regex, sp.P, sp.N)
-    assert re_cost(parse(r.regex), sp.costs) == r.cost
-    assert r.cost <= re_cost(parse(tgt), sp.costs)  # the planted target bounds c*
+        prec = np.all((arr & pw) == pw, axis=1) & np.all((arr & nw) == 0, axis=1)
+        assert not prec.any(), c
+        del arr
+    g.close()
