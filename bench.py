@@ -10,10 +10,14 @@ hot-path row (Q, S, concat, union, precision test, dedup, append, reconstruction
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Under torchrun (N > 1) the ranks run ONE sharded search (every level's
-work lists are partitioned across ranks, new CSs are all-gathered over NCCL and
-merged canonically; "scaling": "strong"); ``--multi replicas`` runs N independent
-searches instead ("scaling": "weak").  Time is the max over ranks.
+With N > 1 (``--gpus N`` spawns its ranks with torch.distributed.run, or runs under
+torchrun) the ranks run ONE sharded search (every large level's work
+lists are partitioned across ranks; the CSs new to a rank go to their hash owners by
+NCCL all-to-all, the owners deduplicate, the uniques are all-gathered; small levels
+run on every rank; "scaling": "strong"); ``--multi replicas`` runs N independent
+searches instead ("scaling": "weak").  Time is the max over ranks.  At N = 1 the line
+also carries a ``secondary`` measurement of BASELINE configs[1] (c2-t1-s0, the HBM
+hash set).
 ``--impl reference`` times the CPU oracle (oracle/, the only reference this tier
 has) on a bounded sample.
 """
@@ -170,6 +174,39 @@ def load_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def load_int_peaks():
+    """Integer-pipe and random-sector ceilings measured on B200 by
+    scripts/microbench/peaks.cu (profiles/r02_peaks_microbench.jsonl)."""
+    out = {"alu_lane_ops_per_clk_per_sm": 64.0, "issue_lane_ops_per_s": None, "alu_lane_ops_per_s": None,
+           "random_reads_per_s": None, "source": "B300_MICROARCH fallback (ALU rt_SMSP = 2)"}
+    path = os.path.join(ROOT, "profiles", "r02_peaks_microbench.jsonl")
+    if not os.path.exists(path):
+        return out
+    rows = [json.loads(l) for l in open(path) if l.strip()]
+    alu = [r["lane_ops_per_s"] for r in rows if r.get("test") == "int_pipe" and r.get("op") == "lop3"]
+    mix = [r["lane_ops_per_s"] for r in rows if r.get("test") == "int_pipe" and r.get("op") == "lop3+imad"]
+    rnd = [r["reads_per_s"] for r in rows if r.get("test") == "random_sector_read" and r.get("table_gib", 0) >= 16]
+    out.update({
+        "alu_lane_ops_per_s": max(alu) if alu else None,
+        "issue_lane_ops_per_s": max(mix) if mix else None,
+        "random_reads_per_s": max(rnd) if rnd else None,
+        "source": "profiles/r02_peaks_microbench.jsonl (scripts/microbench/peaks.cu on one B200)",
+    })
+    return out
+
+
+def host_cpu():
+    """Host CPU model and usable core count (cpu_baseline context)."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:  # noqa: BLE001 -- context only
+        pass
+    return {"model": model, "nproc": os.cpu_count()}
+
+
 def oracle_rate(spec, max_cost):
     import oracle
     t0 = time.perf_counter()
@@ -210,36 +247,83 @@ def run_reference(args, rank):
 
 # ------------------------------------------------------------------ our arm
 
-def run_ours(args, rank, world, local_rank):
+def roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, workload):
+    """Dominant kernel's achieved rate vs its binding ceiling."""
+    dom = max(("concat", "union", "unary", "transpose"), key=lambda k: kstats[k][1])
+    dom_launches, dom_ms = kstats[dom]
+    evaluated = 0
+    for rr in kresults:
+        for l in rr.levels:
+            evaluated += {"concat": l.eval_c, "union": l.eval_u}.get(dom, l.evaluated)
+    s_in = sum(max(0, len(w) - 1) for w in ic_words)
+    peaks, peaks_kind = load_peaks()
+    ip = load_int_peaks()
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    alu_peak = ip["alu_lane_ops_per_s"] or 64 * 148 * sm_mhz * 1e6
+    issue_peak = ip["issue_lane_ops_per_s"] or 128 * 148 * sm_mhz * 1e6
+    opc = ops_per_candidate(dom, w32, s_in)
+    per_s = (evaluated / dom_launches) / (dom_ms / dom_launches / 1000.0) if dom_launches and dom_ms else 0.0
+    achieved = per_s * opc
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get(workload, {}).get(dom)
+    roof = {
+        "bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
+        "frac": achieved / alu_peak, "frac_issue": achieved / issue_peak, "traffic": traffic,
+        "kernel": f"k_{dom}<W32={w32}>", "ops_per_candidate": opc, "candidates_per_s": per_s,
+        "launches": dom_launches, "avg_launch_ms": dom_ms / max(1, dom_launches),
+        "share_of_step": dom_ms / sum(kstep_ms) if world == 1 and kstep_ms else None,
+        "measured_in": kernel_pass,
+        "peak_source": f"INT32 ALU pipe (LOP3/IADD3) measured: {alu_peak:.4g} lane-ops/s = 64/clk/SM "
+                       f"({ip['source']}); frac_issue uses the measured ALU+FMA issue rate "
+                       f"{issue_peak:.4g} lane-ops/s (128/clk/SM)",
+    }
+    if w32 >= 2:
+        # |IC| > 32: the dedup set is an HBM hash table (SURVEY 8(d)): one random 32-byte
+        # sector per probed candidate (the 64-bit key slot), plus the cached entry on a
+        # fingerprint match when keys are indexed (W32 >= 4).  Bound: the measured rate
+        # of random 32-byte reads from a table >> L2 (scripts/microbench/peaks.cu);
+        # the copy-bandwidth fraction is given beside it.
+        sectors = 1 if w32 == 2 else 1 + (4 * w32 + 31) // 32
+        bps = 32 * sectors
+        rnd = ip["random_reads_per_s"] or 36.3e9
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
+        achieved_b = per_s * bps
+        roof.update({
+            "bound": "hbm", "achieved": achieved_b / 1e9, "peak": rnd * 32 / 1e9, "unit": "GB/s",
+            "frac": achieved_b / (rnd * 32), "frac_of_copy_bw": achieved_b / hbm_peak,
+            "bytes_per_candidate": bps, "random_reads_per_s_peak": rnd,
+            "peak_source": f"measured random 32-B reads from a >= 16 GiB table: {rnd:.4g}/s x 32 B "
+                           f"({ip['source']}); copy bandwidth {hbm_peak / 1e9:.0f} GB/s ({peaks_kind})",
+        })
+    return roof
+
+
+def measure(args, workload, rank, world, local_rank, stream, flush, sharded, steps, warmup, primary=True):
+    """Timed solves of one workload (+ sequential kernel pass, e2e through the C ABI)."""
     import torch
     import torch.distributed as dist
-    from paper_2305_18575_b200 import Solver, build
+    from paper_2305_18575_b200 import Solver, nccl_unique_id
 
-    build.build()
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
-    spec, max_cost, desc = WORKLOADS[args.workload]
-    stream = torch.cuda.Stream(device=dev)
-    sharded = world > 1 and args.multi == "shard"
-    mkw = {}
-    if sharded:
+    spec, max_cost, desc = WORKLOADS[workload]
+
+    def nccl_kw():
+        if not sharded:
+            return {}
         # one sharded search over all ranks (SURVEY 8(e)): rank 0's ncclUniqueId is
         # broadcast with torch.distributed; rei_init / rei_solve are then collective
-        from paper_2305_18575_b200 import nccl_unique_id
         box = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(box, src=0)
-        mkw = dict(world_size=world, rank=rank, nccl_id=box[0])
-    multi_note = None
-    # no fallback: a failing multi-GPU init or solve raises (and the run fails)
-    solver = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw)
-    # L2 flush buffer (> 126 MB L2), written between timed steps
-    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
+        return dict(world_size=world, rank=rank, nccl_id=box[0])
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    for _ in range(args.warmup):
+    # no fallback: a failing multi-GPU init or solve raises (and the run fails)
+    solver = Solver.from_spec(spec, device=local_rank, stream=stream, **nccl_kw())
+    for _ in range(warmup):
         r = solver.solve(max_cost)
         assert r.status == "found", r.status
     torch.cuda.synchronize()
@@ -252,7 +336,7 @@ def run_ours(args, rank, world, local_rank):
     sampler = ClockSampler(local_rank)
     sampler.start()
     step_ms, cands, results = [], 0, []
-    for _ in range(args.steps):
+    for _ in range(steps):
         with torch.cuda.stream(stream):
             flush.add_(1)  # write > L2 between timed steps
         barrier()
@@ -269,21 +353,29 @@ def run_ours(args, rank, world, local_rank):
         cands += r.candidates
         results.append(r)
     clocks = sampler.stop()
+    gc.enable()
     launches = solver.launch_count() - launches0
-    kstats = solver.kernel_stats()
+    kstats_timed = solver.kernel_stats()
     ic_words = solver.ic()
     solver.close()  # the kernel pass and the e2e solves below run one context at a time
+    dev = torch.device("cuda", local_rank)
     total_ms, all_cands = reduce_over_ranks(sum(step_ms), cands, dev, world, sum_work=not sharded)
     value = all_cands / (total_ms / 1000.0)
+    w32 = results[0].cs_words
+
+    # SURVEY 8(d) throughput: candidates of the complete levels / their device time
+    comp_c = sum(l.cand for rr in results for l in rr.levels if l.complete == 1)
+    comp_ms = sum(l.ms for rr in results for l in rr.levels if l.complete == 1)
 
     # ---- roofline of the dominant kernel (CUDA events on the launching stream).  In the
-    # timed region a level's kernels overlap on concurrent streams (REI_CONCURRENT 2 or 3),
-    # so one kernel's event span includes SMs lent to another; the per-kernel numbers
-    # come from a sequential pass (REI_CONCURRENT=0, same workload, K steps, L2 flushed)
-    # -- the launch order ncu serialises too.  Concat goes first there (REI_UNION_FIRST=0):
-    # with union first on one stream, a union hit at c* makes the concat launches of that
-    # level exit at once, and their launch overhead would count against the kernel.
-    kresults, kstep_ms, kernel_pass = results, step_ms, "timed region"
+    # timed region a level's kernels overlap on concurrent streams, so one kernel's event
+    # span includes SMs lent to another (the timed-region fraction is a lower bound); the
+    # reported fraction comes from a sequential pass (REI_CONCURRENT=0, same workload,
+    # L2 flushed) -- the launch order ncu serialises too.  Concat goes first there
+    # (REI_UNION_FIRST=0): with union first on one stream, a union hit at c* makes the
+    # concat launches of that level exit at once.
+    roof_timed = roofline_of(kstats_timed, results, step_ms, ic_words, w32, world, "timed region", workload)
+    kresults, kstep_ms, kstats, kernel_pass = results, step_ms, kstats_timed, "timed region"
     if world == 1:
         prev = {k: os.environ.get(k) for k in ("REI_CONCURRENT", "REI_UNION_FIRST")}
         os.environ["REI_CONCURRENT"] = "0"
@@ -300,7 +392,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         ksolver.reset_kernel_stats()
         kresults, kstep_ms = [], []
-        for _ in range(args.steps):
+        for _ in range(steps):
             with torch.cuda.stream(stream):
                 flush.add_(1)
             torch.cuda.synchronize()
@@ -313,67 +405,26 @@ def run_ours(args, rank, world, local_rank):
             kstep_ms.append(e0.elapsed_time(e1))
         kstats = ksolver.kernel_stats()
         ksolver.close()
-        kernel_pass = (f"sequential-stream pass (REI_CONCURRENT=0, REI_UNION_FIRST=0), {args.steps} steps, "
-                       "L2 flushed")
-    dom = max(("concat", "union", "unary", "transpose"), key=lambda k: kstats[k][1])
-    dom_launches, dom_ms = kstats[dom]
-    evaluated = 0
-    for rr in kresults:
-        for l in rr.levels:
-            evaluated += {"concat": l.eval_c, "union": l.eval_u}.get(dom, l.evaluated)
-    w32 = results[0].cs_words
-    s_in = sum(max(0, len(w) - 1) for w in ic_words)
-    peaks, peaks_kind = load_peaks()
-    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    alu_peak = 64 * 148 * sm_mhz * 1e6  # INT32 ALU-pipe lane-ops/s (B300_MICROARCH rt_SMSP=2)
-    opc = ops_per_candidate(dom, w32, s_in)
-    achieved = (evaluated / dom_launches) * opc / (dom_ms / dom_launches / 1000.0) if dom_launches else 0.0
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
-    if os.path.exists(tpath):
-        t = json.load(open(tpath))
-        traffic = t.get(args.workload, {}).get(dom)
-    roofline = {
-        "bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
-        "frac": achieved / alu_peak, "traffic": traffic, "kernel": f"k_{dom}<W32={w32}>",
-        "ops_per_candidate": opc, "launches": dom_launches, "avg_launch_ms": dom_ms / max(1, dom_launches),
-        "share_of_step": dom_ms / sum(kstep_ms) if world == 1 else None,
-        "measured_in": kernel_pass,
-        "peak_source": f"64 INT32 lane-ops/clk/SM x 148 SMs x {sm_mhz:.0f} MHz ({peaks_kind} sm_max_mhz)",
-        "hbm_peak_gbs": peaks.get("hbm_gbs"),
-    }
-    if w32 >= 2:
-        # |IC| > 32: the dedup set is an HBM hash table: the algorithmic
-        # traffic is one random 32-byte sector per probed candidate (the 64-bit key
-        # slot), plus the cached entry for a fingerprint match when keys are indexed
-        # (W32 >= 4); bound = measured HBM bandwidth
-        sectors = 1 if w32 == 2 else 1 + (4 * w32 + 31) // 32
-        bps = 32 * sectors
-        hbm_peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
-        achieved_b = (evaluated / dom_launches) * bps / (dom_ms / dom_launches / 1000.0) if dom_launches else 0.0
-        roofline.update({
-            "bound": "hbm", "achieved": achieved_b / 1e9, "peak": hbm_peak / 1e9, "unit": "GB/s",
-            "frac": achieved_b / hbm_peak, "bytes_per_candidate": bps, "ops_per_candidate": None,
-            "peak_source": f"{peaks_kind} hbm_gbs (MEASURED_PEAKS.json)",
-            "note": "random 32-B sectors: a fully random-access workload reaches only part of the copy bandwidth",
-        })
+        kernel_pass = f"sequential-stream pass (REI_CONCURRENT=0, REI_UNION_FIRST=0), {steps} steps, L2 flushed"
+    roofline = roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, workload)
+    roofline["frac_timed_region"] = roof_timed["frac"]
+    roofline["kernel_timed_region"] = roof_timed["kernel"]
 
     # ---- end to end through the public API with host buffers (rei_init + rei_solve + result)
+    e2e = None
+    n_e2e = max(1, min(steps, 5))
     e2e_s, e2e_cands, h2d, d2h = 0.0, 0, 0, 0
     init_ms, solve_ms = [], []
-    n_e2e = max(1, min(args.steps, 5))
+    gc.collect()
+    gc.disable()
     for rep in range(n_e2e + 1):  # rep 0: untimed warm-up (first context on the pool)
         with torch.cuda.stream(stream):
             flush.add_(1)
         torch.cuda.synchronize()
+        kw = nccl_kw()
         barrier()
         t0 = time.perf_counter()
-        mkw2 = {}
-        if sharded:
-            box = [nccl_unique_id() if rank == 0 else None]
-            dist.broadcast_object_list(box, src=0)
-            mkw2 = dict(world_size=world, rank=rank, nccl_id=box[0])
-        s2 = Solver.from_spec(spec, device=local_rank, stream=stream, **mkw2)
+        s2 = Solver.from_spec(spec, device=local_rank, stream=stream, **kw)
         t_init = time.perf_counter()
         r2 = s2.solve(max_cost)
         _ = r2.regex  # result already copied to the host by rei_solve
@@ -390,52 +441,95 @@ def run_ours(args, rank, world, local_rank):
         h2d += hb
         d2h += db
     gc.enable()
-    e2e = {"value": e2e_cands / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d // n_e2e,
+    e2e_t, e2e_c = reduce_over_ranks(1000 * e2e_s, e2e_cands, dev, world, sum_work=not sharded)
+    e2e = {"value": e2e_c / (e2e_t / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d // n_e2e,
            "d2h_bytes_per_step": d2h // n_e2e,
-           "time_to_minimal_re_ms": 1000 * e2e_s / n_e2e,
+           "time_to_minimal_re_ms": e2e_t / n_e2e,
            "init_ms_median": statistics.median(init_ms), "solve_ms_median": statistics.median(solve_ms),
            "init_ms": [round(x, 3) for x in init_ms], "solve_ms": [round(x, 3) for x in solve_ms],
            "warmup_reps": 1,
            "note": "rei_init (host strings -> device precompute) + rei_solve + result, host wall clock"}
+    r0 = results[-1]
+    return {
+        "value": value, "total_ms": total_ms, "cands": cands, "results": results, "step_ms": step_ms,
+        "roofline": roofline, "e2e": e2e, "launches": launches, "clocks": clocks, "desc": desc,
+        "max_cost": max_cost, "spec": spec,
+        "complete_levels": {"value": comp_c / (comp_ms / 1000.0) if comp_ms else None, "unit": UNIT,
+                            "candidates_per_step": comp_c / steps, "device_ms_per_step": comp_ms / steps,
+                            "note": "SURVEY 8(d): candidates of complete levels / their device time "
+                                    "(CUDA events per level)"},
+        "config": {
+            "workload": workload, "description": desc, "max_cost": max_cost,
+            "n_ic": r0.n_ic, "cs_bits": 32 * r0.cs_words, "cstar": r0.cost, "regex": r0.regex,
+            "candidates_per_step": cands / steps,
+            "candidates_through_last_complete_level": r0.cand_complete,
+            "time_to_minimal_re_ms": statistics.median(step_ms),
+            "time_to_minimal_re_ms_all": [round(x, 3) for x in step_ms],
+        },
+    }
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    from paper_2305_18575_b200 import build
+
+    build.build()
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.Stream(device=dev)
+    sharded = world > 1 and args.multi == "shard"
+    # L2 flush buffer (> 126 MB L2), written between timed steps
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device=dev)
+    m = measure(args, args.workload, rank, world, local_rank, stream, flush, sharded, args.steps, args.warmup)
 
     # ---- CPU oracle baseline (rank 0, N=1 only, bounded sample)
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         mc = ORACLE_SAMPLE_COST[args.workload]
-        c, dt, _ = oracle_rate(spec, mc)
+        c, dt, _ = oracle_rate(m["spec"], mc)
+        hc = host_cpu()
         cpu_baseline = {"value": c / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+                        "host_cpu": hc["model"], "host_nproc": hc["nproc"],
                         "sample": f"oracle/rei_oracle.cpp levels 1..{mc} of {args.workload}: "
-                                  f"{c} candidates in {dt:.1f} s on 1 host core"}
+                                  f"{c} candidates in {dt:.1f} s on 1 host core ({hc['model']})"}
+
+    # ---- secondary workload (N=1): BASELINE configs[1], the HBM hash set (the headline
+    # C5 workload dedups in an L2-resident bitmap)
+    secondary = None
+    if world == 1 and args.secondary and args.secondary != args.workload:
+        s = measure(args, args.secondary, rank, world, local_rank, stream, flush, False,
+                    max(3, args.steps // 2), 3)
+        secondary = {"workload": args.secondary, "metric": METRIC, "value": s["value"], "unit": UNIT,
+                     "ms_per_step": s["total_ms"] / max(1, len(s["step_ms"])), "config": s["config"],
+                     "roofline": s["roofline"], "e2e": s["e2e"], "complete_levels": s["complete_levels"],
+                     "gpu_launches": s["launches"], "clocks": s["clocks"]}
 
     paper = PAPER.get(args.workload)
     vs = None
     if paper:
-        vs = value / (paper["reps"] / paper["gpu_s"])
-    r0 = results[-1]
+        vs = m["value"] / (paper["reps"] / paper["gpu_s"])
+    cfg = dict(m["config"])
+    cfg.update({
+        "l2": f"{args.flush_mb} MiB buffer written between timed steps (L2 flush)",
+        "parallelism": (f"shard{world} (level work lists partitioned; hash-owner NCCL all-to-all, "
+                        "owner dedup, all-gather of the uniques)" if sharded else f"replicas{world}")
+        if world > 1 else "single",
+        "paper_context": paper,
+        "vs_baseline_note": "value / paper's |REs| per GPU-second on A100 for this spec; the paper's "
+                            "|REs| counting convention differs from reading A9 (DESIGN.md)" if paper else None,
+    })
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "metric": METRIC, "value": m["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": m["total_ms"] / args.steps, "higher_is_better": True,
         "scaling": "strong" if sharded else "weak", "vs_baseline": vs, "dtype": "u32", "data": "synthetic",
-        "config": {
-            "workload": args.workload, "description": desc, "max_cost": max_cost,
-            "n_ic": r0.n_ic, "cs_bits": 32 * r0.cs_words, "cstar": r0.cost, "regex": r0.regex,
-            "candidates_per_step": cands / args.steps,
-            "candidates_through_last_complete_level": r0.cand_complete,
-            "time_to_minimal_re_ms": statistics.median(step_ms),
-            "l2": f"{args.flush_mb} MiB buffer written between timed steps (L2 flush)",
-            "parallelism": (f"shard{world} (level work lists partitioned; hash-owner NCCL all-to-all, "
-                            "owner dedup, all-gather of the uniques)"
-                            if sharded else f"replicas{world}") if world > 1 else "single",
-            "multi_note": multi_note,
-            "paper_context": paper,
-            "vs_baseline_note": "value / paper's |REs| per GPU-second on A100 for this spec; the paper's "
-                                "|REs| counting convention differs from reading A9 (DESIGN.md)" if paper else None,
-        },
-        "roofline": roofline,
+        "config": cfg,
+        "roofline": m["roofline"],
         "cpu_baseline": cpu_baseline,
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clocks,
+        "e2e": m["e2e"],
+        "complete_levels": m["complete_levels"],
+        "gpu_launches": m["launches"],
+        "clocks": m["clocks"],
+        "secondary": secondary,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -451,6 +545,8 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="table1-row1")
     ap.add_argument("--flush-mb", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--secondary", default="c2-t1-s0",
+                    help="N=1: also measure this workload (BASELINE configs[1], HBM hash set); '' = off")
     ap.add_argument("--multi", choices=["shard", "replicas"], default="shard",
                     help="N > 1: one sharded search (default) or N independent replicas")
     args = ap.parse_args()
