@@ -550,6 +550,10 @@ def main():
     ap.add_argument("--multi", choices=["shard", "replicas"], default="shard",
                     help="N > 1: one sharded search (default) or N independent replicas")
     args = ap.parse_args()
+    if args.secondary in ("", "none", "off"):
+        args.secondary = None
+    elif args.secondary not in WORKLOADS:
+        raise SystemExit(f"--secondary {args.secondary}: not a workload ({', '.join(sorted(WORKLOADS))})")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `bench.py --gpus N` without a launcher: become N ranks (one process per GPU)
         # under torch.distributed.run on this node

@@ -47,6 +47,15 @@ std::map<void*, size_t> g_host_size;                      // every pinned block 
 
 size_t round_up(size_t b) { return (b + kGran - 1) / kGran * kGran; }
 
+// Free-memory estimate per device: one cudaMemGetInfo (0.3-70 ms on B200, measured),
+// then this allocator's own cudaMalloc / cudaFree traffic since that query.
+struct FreeInfo {
+  bool known = false;
+  uint64_t free_at_query = 0;
+  int64_t net_since = 0;  // bytes cudaMalloc'd minus bytes cudaFree'd since the query
+};
+std::map<int, FreeInfo> g_free_info;
+
 // Take a cached block of at least `bytes` (<= bytes + bytes/8) on `dev`; nullptr if none.
 void* take_cached(int dev, size_t bytes) {
   auto& fl = g_dev_free[dev];
@@ -62,6 +71,7 @@ void release_device(int dev) {  // caller holds g_mu
   for (auto& kv : fl) {
     cudaFree(kv.second);
     g_dev_blocks.erase(kv.second);
+    g_free_info[dev].net_since -= (int64_t)kv.first;
   }
   fl.clear();
 }
@@ -95,7 +105,32 @@ cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
     return e;
   }
   g_dev_blocks[*p] = {dev, want};
+  g_free_info[dev].net_since += (int64_t)want;
   return cudaSuccess;
+}
+
+uint64_t dev_free_estimate(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  FreeInfo& fi = g_free_info[dev];
+  if (!fi.known) {
+    size_t fr = 0, tot = 0;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != dev) cudaSetDevice(dev);
+    cudaMemGetInfo(&fr, &tot);
+    if (cur != dev) cudaSetDevice(cur);
+    fi = FreeInfo{true, (uint64_t)fr, 0};
+  }
+  int64_t est = (int64_t)fi.free_at_query - fi.net_since;
+  auto it = g_dev_free.find(dev);
+  if (it != g_dev_free.end())
+    for (auto& kv : it->second) est += (int64_t)kv.first;  // idle blocks can be released
+  return est > 0 ? (uint64_t)est : 0;
+}
+
+void dev_free_estimate_reset(int dev) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  g_free_info[dev].known = false;
 }
 
 void dev_free(void* p, cudaStream_t st) {

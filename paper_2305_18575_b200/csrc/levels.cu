@@ -242,6 +242,93 @@ __device__ __forceinline__ bool insert_hash64(const S& p, unsigned long long key
   return false;
 }
 
+// ---- dedup: inline wide keys (DEDUP_HASHIN, W32 = 4 or 8).  A slot is the CS itself
+// as W/2 u64 words; empty = all ones.  W32 = 4 (|IC| <= 127): one 16-byte CAS claims
+// the slot with the whole key.  W32 = 8 (|IC| <= 254): the slot's first 16 bytes hold
+// the key's HIGH half (u64 words 2, 3), claimed by a 16-byte CAS with bit 62 of word 3
+// set ("second half pending"; bits 254/255 of a CS are never set, so a claimed slot is
+// never all ones); the owner then stores the low half and clears the pending bit.
+// Readers that match the high half wait for the pending bit, then compare the low half.
+constexpr unsigned long long kPend = 1ull << 62;
+
+__device__ __forceinline__ void ld16(const unsigned long long* a, unsigned long long& x, unsigned long long& y) {
+  const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(a);
+  x = v.x;
+  y = v.y;
+}
+__device__ __forceinline__ void ld16v(const unsigned long long* a, unsigned long long& x, unsigned long long& y) {
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(x), "=l"(y) : "l"(a) : "memory");
+}
+__device__ __forceinline__ void st16v(unsigned long long* a, unsigned long long x, unsigned long long y) {
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(a), "l"(x), "l"(y) : "memory");
+}
+// 16-byte compare-and-swap (sm_90+ atom.cas.b128); returns the old value
+__device__ __forceinline__ void cas16(unsigned long long* a, unsigned long long c0, unsigned long long c1,
+                                      unsigned long long v0, unsigned long long v1, unsigned long long& o0,
+                                      unsigned long long& o1) {
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.global.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(o0), "=l"(o1)
+      : "l"(c0), "l"(c1), "l"(v0), "l"(v1), "l"(a)
+      : "memory");
+}
+
+// the inline key of a CS: the claimed half first (W32 = 8: high half)
+template <int W>
+__device__ __forceinline__ void inline_key(const uint32_t (&cs)[W], unsigned long long (&k)[W / 2]) {
+  static_assert(W == 4 || W == 8, "inline keys are 16 or 32 bytes");
+#pragma unroll
+  for (int q = 0; q < W / 2; ++q) {
+    const int src = (W == 8) ? ((q + 2) & 3) : q;  // W = 8: words 2, 3, 0, 1
+    k[q] = ((unsigned long long)cs[2 * src + 1] << 32) | cs[2 * src];
+  }
+}
+
+// Resolve the insert of an inline key whose slot `s` head (16 B) is already loaded.
+template <int W, class S>
+__device__ bool insert_inline(const S& p, const unsigned long long (&k)[W / 2], unsigned long long s,
+                              unsigned long long v0, unsigned long long v1) {
+  constexpr int U = W / 2;  // u64 words per slot
+  for (int probe = 0; probe < kMaxProbe; ++probe) {
+    unsigned long long* slot = p.dedup.table + s * U;
+    if (v0 == ~0ull && v1 == ~0ull) {  // empty: claim it
+      if (*(volatile unsigned int*)&p.ctl->overflow) return false;
+      unsigned long long o0, o1;
+      cas16(slot, ~0ull, ~0ull, k[0], (W == 8) ? (k[1] | kPend) : k[1], o0, o1);
+      if (o0 == ~0ull && o1 == ~0ull) {
+        if (W == 8) {
+          st16v(slot + 2, k[U > 2 ? 2 : 0], k[U > 2 ? 3 : 1]);
+          __threadfence();
+          atomicAnd(slot + 1, ~kPend);
+        }
+        return true;
+      }
+      v0 = o0;
+      v1 = o1;
+      continue;  // re-examine the slot with the value that won
+    }
+    if (v0 == k[0] && (v1 & ~(W == 8 ? kPend : 0ull)) == k[1]) {
+      if (W == 4) return false;
+      while (v1 & kPend) {  // the owner is writing the low half
+        __nanosleep(20);
+        v1 = *(volatile unsigned long long*)(slot + 1);
+      }
+      __threadfence();
+      unsigned long long w0, w1;
+      ld16v(slot + 2, w0, w1);
+      if (w0 == k[U > 2 ? 2 : 0] && w1 == k[U > 2 ? 3 : 1]) return false;
+    }
+    s = (s + 1) & p.dedup.mask;
+    ld16(p.dedup.table + s * U, v0, v1);
+  }
+  p.ctl->overflow = 1;
+  return false;
+}
+
 // Bitmap position of a one-word CS (dedup over all 2^n languages, |IC| <= 32): the
 // n-bit CS bit-reversed.  The bits of the long IC words (high CS bits) are the ones
 // that vary most among the 32 candidates of a warp group (one uniform operand x 32
@@ -359,8 +446,18 @@ __device__ __noinline__ bool sharded_new(const Peer* __restrict__ peers, uint32_
   const unsigned long long h = hash_cs<W>(cs);
   const Peer& o = peers[(uint32_t)(h >> 40) % shards];
   constexpr int MODE = DedupOf<W>::mode;
-  if (MODE == DEDUP_HASHIDX) return insert_indexed<W>(o, cs, rank, true, 0);
   bool isnew;
+  if constexpr (W == 4 || W == 8) {
+    if (o.dedup.mode == DEDUP_HASHIN) {
+      unsigned long long key[W / 2], v0, v1;
+      inline_key<W>(cs, key);
+      const unsigned long long slot = h & o.dedup.mask;
+      ld16v(o.dedup.table + slot * (W / 2), v0, v1);
+      isnew = insert_inline<W>(o, key, slot, v0, v1);
+      goto appended;
+    }
+  }
+  if (MODE == DEDUP_HASHIDX) return insert_indexed<W>(o, cs, rank, true, 0);
   if (MODE == DEDUP_BITMAP) {
     const uint32_t pos = bm_pos(cs[0], n);
     const uint32_t bit = 1u << (pos & 31);
@@ -369,6 +466,7 @@ __device__ __noinline__ bool sharded_new(const Peer* __restrict__ peers, uint32_
     const unsigned long long slot = h & o.dedup.mask;
     isnew = insert_hash64(o, key64<W>(cs), slot, *(volatile unsigned long long*)&o.dedup.table[slot]);
   }
+appended:
   if (!isnew) return false;
   const unsigned long long idx = o.out_base + atomicAdd(&o.ctl->count, 1ull);
   if (idx >= o.cap) {
@@ -489,6 +587,26 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
         stage_push<W>(p, *stage, isnew[g], cs[g], r);
       } else if (isnew[g]) {
         on_new<W>(p, cs[g], rank_of, g);
+      }
+    }
+  } else if (p.dedup.mode == DEDUP_HASHIN) {
+    if constexpr (W == 4 || W == 8) {
+      // inline wide keys: the G slot heads are loaded before any is resolved
+      unsigned long long key[G][W / 2], slot[G], v0[G], v1[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        inline_key<W>(cs[g], key[g]);
+        slot[g] = hash_cs<W>(cs[g]) & p.dedup.mask;
+        v0[g] = key[g][0];
+        v1[g] = key[g][1];
+        if (valid[g] && !skip[g]) ld16(p.dedup.table + slot[g] * (W / 2), v0[g], v1[g]);
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        if (!valid[g] || skip[g]) continue;
+        // W32 = 4: a head equal to the key is a hit without leaving the register file
+        if (W == 4 && v0[g] == key[g][0] && v1[g] == key[g][1]) continue;
+        if (insert_inline<W>(p, key[g], slot[g], v0[g], v1[g])) on_new<W>(p, cs[g], rank_of, g);
       }
     }
   } else {
@@ -665,9 +783,15 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
   uint32_t* myX = myT + NW;  // the uniform operand (W > 2)
   constexpr int G = Batch<W>::G;
 
-  uint32_t nspl[W];
+  uint32_t nspl[W], kq[W];
 #pragma unroll
-  for (int q = 0; q < W; ++q) nspl[q] = s_nsplit[q * 32 + lane];
+  for (int q = 0; q < W; ++q) {
+    nspl[q] = s_nsplit[q * 32 + lane];
+    // row q = words 32q .. 32q + 31 (nearly equal lengths in shortlex order): the fold
+    // runs to the row's longest split list, and rows past |IC| are all zero
+    kq[q] = __reduce_max_sync(kFull, nspl[q]);
+  }
+  const uint32_t rows = (p.n + 31) / 32;  // live CS rows (warp-uniform)
 
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
@@ -724,7 +848,19 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
           uint32_t acc[W];
 #pragma unroll
           for (int q = 0; q < W; ++q) acc[q] = (xeps ? T[q] : 0u) | (((x[q] >> lane) & 1u) ? Teps : 0u);
-          for (uint32_t k = 0; k < p.maxk; ++k) {
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            if (kShfl || (uint32_t)q >= rows) continue;  // (W <= 2: the loop below)
+            for (uint32_t k = 0; k < kq[q]; ++k) {
+              const uint32_t sp = s_split[k * NW + q * 32 + lane];
+              const uint32_t ufix = slice_a ? (sp & 0xffffu) : (sp >> 16);
+              const uint32_t vsl = slice_a ? (sp >> 16) : (sp & 0xffffu);
+              const uint32_t t = myT[vsl & (NW - 1)];
+              const uint32_t xb = (myX[(ufix >> 5) & (W - 1)] >> (ufix & 31)) & 1u;
+              if (k < nspl[q] && xb) acc[q] |= t;
+            }
+          }
+          for (uint32_t k = 0; kShfl && k < p.maxk; ++k) {
 #pragma unroll
             for (int q = 0; q < W; ++q) {
               const uint32_t sp = s_split[k * NW + q * 32 + lane];
@@ -748,7 +884,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
             }
           }
 #pragma unroll
-          for (int q = 0; q < W; ++q) cs[g][q] = transpose32(acc[q], lane);
+          for (int q = 0; q < W; ++q) cs[g][q] = (kShfl || (uint32_t)q < rows) ? transpose32(acc[q], lane) : 0u;
           valid[g] = active && lane_ok;
           skip[g] = cs_equal<W>(cs[g], x);  // equals a cached operand: old
           evaluated += valid[g] ? 1u : 0u;
@@ -1356,6 +1492,96 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
   if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
 }
 
+// Bit-sliced unary kernel for wide CSs (W32 >= 4, |IC| > 64): a warp takes a slab of
+// 32 operands.  The slab's transposed words X[w] (bit t = operand t's bit w) and the
+// star slices S[w] live in the warp's shared memory; round L computes every word of
+// length L (a contiguous shortlex range) spread over the lanes,
+//   S[w] = X[w] | OR_{proper (u,v) of w} X[u] & S[v],   S[eps] = all ones,
+// where v is shorter than w, so S[v] is final (same fixpoint as star_cs: P:636,
+// P:641-642).  Per slab that is S_in shared-memory AND/ORs for 32 operands, against
+// S_in bit tests of W-word registers per operand in k_unary.  W transposes turn the
+// slices into the 32 stars (one per lane).  ? is x | eps per lane.
+template <int W>
+__global__ void __launch_bounds__(256) k_unary_wide(LevelParams p, unsigned long long n_q, unsigned long long n_s,
+                                                   unsigned long long base_q, unsigned long long base_s,
+                                                   unsigned long long slab_s) {
+  constexpr int NW = 32 * W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  uint32_t* sX = reinterpret_cast<uint32_t*>(smem_raw) + warp * 2 * NW;
+  uint32_t* sS = sX + NW;
+  constexpr uint32_t kLen = kMaxSplitRows + 3;  // word lengths 0 .. kMaxSplitRows + 1
+  __shared__ uint32_t s_lstart[kLen + 1];          // first word of each length (shortlex)
+  if (threadIdx.x == 0) {
+    uint32_t L = 0;
+    for (uint32_t w = 0; w < p.n; ++w)
+      while (L < kLen && L <= p.word_len[w]) s_lstart[L++] = w;
+    while (L <= kLen) s_lstart[L++] = p.n;
+  }
+  __syncthreads();
+  uint32_t maxlen = 0;
+  while (maxlen + 1 < kLen && s_lstart[maxlen + 1] < p.n) ++maxlen;
+
+  const unsigned long long total = n_q + n_s;
+  const unsigned long long tb = p.item_begin;  // this rank's operand share [tb, te)
+  const unsigned long long te = total < (unsigned long long)p.total_items ? total : (unsigned long long)p.total_items;
+  const unsigned long long slabs_q = (n_q + 31) / 32, slabs_s = (n_s + 31) / 32;
+  const unsigned long long gwarp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  uint32_t evaluated = 0;
+  const unsigned long long nslab = slabs_q + slabs_s;
+  for (unsigned long long it = gwarp; it < nslab; it += nwarps) {
+    const bool star = it >= slabs_q;
+    const unsigned long long s = star ? it - slabs_q : it;
+    const unsigned long long cnt = star ? n_s : n_q;
+    const unsigned long long first = (star ? n_q : 0) + s * 32;  // unary rank of lane 0
+    if (first >= te || first + 32 <= tb) continue;  // warp-uniform
+    const unsigned long long i = s * 32 + lane;  // operand index within its level
+    const bool valid = i < cnt && first + lane >= tb && first + lane < te;
+    uint32_t x[W], cs[1][W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) x[q] = 0;
+    if (i < cnt) load_cs<W>(p.arena, (star ? base_s : base_q) + i, x);
+    if (!star) {
+#pragma unroll
+      for (int q = 0; q < W; ++q) cs[0][q] = x[q];
+      cs[0][0] |= 1u;  // x? = eps + x
+    } else {
+      const uint32_t* T = p.tarena + (slab_s + s) * NW;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        sX[q * 32 + lane] = T[q * 32 + lane];
+        sS[q * 32 + lane] = 0u;
+      }
+      __syncwarp();
+      if (lane == 0) sS[0] = kFull;  // every star contains eps
+      for (uint32_t L = 1; L <= maxlen; ++L) {
+        __syncwarp();
+        const uint32_t w1 = s_lstart[L + 1];
+        for (uint32_t w = s_lstart[L] + lane; w < w1; w += 32) {
+          uint32_t acc = sX[w];
+          for (uint32_t k = 0; k + 1 < L; ++k) {
+            const uint32_t sp = __ldg(&p.split[(size_t)k * kMaxNW + w]);
+            acc |= sX[sp >> 16] & sS[sp & 0xffffu];
+          }
+          sS[w] = acc;
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < W; ++q) cs[0][q] = transpose32(sS[q * 32 + lane], lane);
+      __syncwarp();
+    }
+    bool vv[1] = {valid}, skip[1] = {cs_equal<W>(cs[0], x)};
+    evaluated += valid ? 1u : 0u;
+    const unsigned long long rk = p.rank_base + first + lane;
+    process_batch<W, 1>(p, cs, vv, skip, [&](int) { return rk; });
+  }
+  const uint32_t tot = __reduce_add_sync(kFull, evaluated);
+  if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
+}
+
 // Seeds (Alg. 1 line 3): one thread, symbols in Sigma order (deterministic).
 template <int W>
 __global__ void k_seeds(LevelParams p, const uint32_t* seeds, int nsym) {
@@ -1409,6 +1635,14 @@ __global__ void k_rehash(LevelParams p, unsigned long long base, unsigned long l
       const unsigned long long key = key64<W>(x);
       const unsigned long long s = hash_cs<W>(x) & p.dedup.mask;
       insert_hash64(p, key, s, p.dedup.table[s]);
+    } else if (p.dedup.mode == DEDUP_HASHIN) {
+      if constexpr (W == 4 || W == 8) {
+        unsigned long long key[W / 2], v0, v1;
+        inline_key<W>(x, key);
+        const unsigned long long s = hash_cs<W>(x) & p.dedup.mask;
+        ld16v(p.dedup.table + s * (W / 2), v0, v1);
+        insert_inline<W>(p, key, s, v0, v1);
+      }
     } else {
       insert_indexed<W>(p, x, 0, false, t);
     }
@@ -1476,7 +1710,7 @@ int sm_count() {
 
 template <typename K>
 int grid_for(K kernel, int threads, size_t smem, unsigned long long work_units_per_cta_hint,
-             unsigned long long work) {
+             unsigned long long work, int waves = 1) {
   // the occupancy query costs host microseconds per launch: cache it per (kernel, smem)
   thread_local std::unordered_map<unsigned long long, int> cache;
   const unsigned long long key = (unsigned long long)(uintptr_t)(const void*)kernel ^ ((unsigned long long)smem << 48);
@@ -1490,7 +1724,7 @@ int grid_for(K kernel, int threads, size_t smem, unsigned long long work_units_p
   }
   if (occ <= 0) occ = 1;
   unsigned long long want = (work + work_units_per_cta_hint - 1) / work_units_per_cta_hint;
-  unsigned long long full = (unsigned long long)sm_count() * occ;
+  unsigned long long full = (unsigned long long)sm_count() * occ * (unsigned long long)waves;
   if (want < 1) want = 1;
   return (int)std::min<unsigned long long>(want, full);
 }
@@ -1500,6 +1734,18 @@ size_t pair_smem(const LevelParams& p, int W) {
   size_t s = p.nblocks * sizeof(Block) + (size_t)p.maxk * NW * 4 + NW * 4;
   if (W > 2) s += (size_t)kWarps * (NW + W) * 4;
   return s;
+}
+
+// Concat grids span this many waves of resident CTAs (REI_CONCAT_WAVES, default 16; 1 =
+// persistent): with more than one, CTAs retire during the level and the union kernel of
+// a concurrent level (higher stream priority) gets SMs even when concat reached them first.
+int concat_waves() {
+  const char* e = getenv("REI_CONCAT_WAVES");
+  return e ? std::max(1, atoi(e)) : 16;
+}
+int union_waves() {
+  const char* e = getenv("REI_UNION_WAVES");
+  return e ? std::max(1, atoi(e)) : 1;
 }
 
 template <int W, int MAXK, bool SA>
@@ -1512,7 +1758,8 @@ int launch_concat_fast_t(const LevelParams& p, cudaStream_t st) {
 #ifdef REI_CARVEOUT
   cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributePreferredSharedMemoryCarveout, REI_CARVEOUT);
 #endif
-  const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
+  const int grid = grid_for(k_concat_fast<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin,
+                            concat_waves());
   k_concat_fast<W, MAXK, SA><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
@@ -1532,7 +1779,7 @@ int launch_concat_generic(const LevelParams& p, cudaStream_t st) {
   const size_t smem = pair_smem(p, W);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_concat<W, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int grid = grid_for(k_concat<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
+  const int grid = grid_for(k_concat<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin, concat_waves());
   k_concat<W, SH><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
@@ -1555,7 +1802,7 @@ int launch_union_sh(const LevelParams& p, cudaStream_t st) {
 #ifdef REI_CARVEOUT
   cudaFuncSetAttribute(k_union<W, SH>, cudaFuncAttributePreferredSharedMemoryCarveout, REI_CARVEOUT);
 #endif
-  const int grid = grid_for(k_union<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin);
+  const int grid = grid_for(k_union<W, SH>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin, union_waves());
   k_union<W, SH><<<grid, kWarps * 32, smem, st>>>(p);
   return 1;
 }
@@ -1593,6 +1840,15 @@ int launch_unary_t(const LevelParams& p, unsigned long long n_q, unsigned long l
       if (p.maxk <= 3) return launch_unary_fast_t<W, 3>(p, n_q, n_s, bq, bs, slab_s, st);
       if (p.maxk <= 7) return launch_unary_fast_t<W, 7>(p, n_q, n_s, bq, bs, slab_s, st);
       return launch_unary_fast_t<W, 15>(p, n_q, n_s, bq, bs, slab_s, st);
+    }
+  }
+  if constexpr (W >= 4) {
+    if (!getenv("REI_GENERIC_UNARY")) {
+      const unsigned long long slabs = (n_q + 31) / 32 + (n_s + 31) / 32;
+      const size_t smem = (size_t)8 * 2 * 32 * W * 4;  // per warp: X and S slices
+      const int grid = grid_for(k_unary_wide<W>, 256, smem, 8, slabs);
+      k_unary_wide<W><<<grid, 256, smem, st>>>(p, n_q, n_s, bq, bs, slab_s);
+      return 1;
     }
   }
   const size_t smem = (size_t)p.maxk * 32 * W * 4 + 32 * W * 4;

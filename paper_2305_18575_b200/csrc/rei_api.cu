@@ -118,7 +118,8 @@ struct Ctx {
   rei_costs costs{};
   uint32_t err_num = 0, err_den = 1;
   uint32_t flags = 0;
-  uint64_t budget = 0;       // 0 until first needed (budget_of)
+  uint64_t budget = 0;       // user budget, or (sharded) the driver's free memory once queried
+  bool budget_user = false;  // rei_options.mem_budget_bytes was given
   uint64_t budget_used = 0;  // bytes allocated before the budget was first queried
   uint64_t entry_limit = 0;  // rei_options.max_entries (0 = budget only)
   int otf_level = 0;         // first level checked in OnTheFly mode (0 = none)
@@ -267,17 +268,22 @@ struct Ctx {
     pending.push_back(ep);
   }
   // after a stream sync: fold the pending event pairs into the per-class totals
+  // level_ms = the wall span of the pending launches (first start to last end): a
+  // level's kernels may overlap on the auxiliary streams, so their sum would overcount
   void collect_events(double* level_ms) {
-    double tot = 0;
+    float lo = 0, hi = 0;
     for (auto& ep : pending) {
-      float ms = 0;
+      float ms = 0, a = 0, b = 0;
       cudaEventElapsedTime(&ms, ep.a, ep.b);
       k_ms[ep.cls] += ms;
-      tot += ms;
+      cudaEventElapsedTime(&a, pending[0].a, ep.a);
+      cudaEventElapsedTime(&b, pending[0].a, ep.b);
+      lo = std::min(lo, a);
+      hi = std::max(hi, b);
     }
     pending.clear();
     ev_next = 0;
-    if (level_ms) *level_ms = tot;
+    if (level_ms) *level_ms = hi - lo;
   }
 };
 
@@ -297,23 +303,36 @@ int next_pow2_words(int n) {
   return p;
 }
 
+// bytes per dedup-set slot: an 8-byte key / index word, or the whole CS (inline keys)
+uint64_t slot_bytes(const Ctx* c) { return c->mode == DEDUP_HASHIN ? 4ull * c->W32 : 8ull; }
+
 uint64_t bytes_per_entry(const Ctx* c) {
   // CS + back-pointer + transposed copy (+ hash slots at load <= 1/2)
   uint64_t b = 4ull * c->W32 + 8 + 4ull * c->W32;
-  if (c->mode != DEDUP_BITMAP) b += 16;
+  if (c->mode != DEDUP_BITMAP) b += 2 * slot_bytes(c);
   return b;
 }
 
-// (Re)allocate arena, bp, tarena for `cap` entries, preserving the first `keep` entries.
+// (Re)allocate arena, bp, tarena (and the dedup table) for `cap` entries, preserving the
+// first `keep` entries.  Out of device memory: REI_OUT_OF_MEMORY with the previous
+// buffers unchanged (or, if only the new table failed, a table of the previous size and
+// the previous capacity), so the caller can fall back to OnTheFly mode.
 rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_slabs) {
   const uint64_t new_slab_cap = new_cap / 32 + 4096;
   uint32_t* a = nullptr;
   unsigned long long* b = nullptr;
   uint32_t* t = nullptr;
   const auto t0 = std::chrono::steady_clock::now();
-  CUDA_OK(c, c->dmalloc(&a, new_cap * 4ull * c->W32));
-  CUDA_OK(c, c->dmalloc(&b, new_cap * 8ull));
-  CUDA_OK(c, c->dmalloc(&t, new_slab_cap * 32ull * c->W32 * 4ull));
+  auto oom = [&](cudaError_t e, const char* what) {
+    c->dfree(a); c->dfree(b); c->dfree(t);
+    cudaGetLastError();
+    c->err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? REI_OUT_OF_MEMORY : REI_ECUDA;
+  };
+  cudaError_t e;
+  if ((e = c->dmalloc(&a, new_cap * 4ull * c->W32)) != cudaSuccess) return oom(e, "arena allocation");
+  if ((e = c->dmalloc(&b, new_cap * 8ull)) != cudaSuccess) return oom(e, "back-pointer allocation");
+  if ((e = c->dmalloc(&t, new_slab_cap * 32ull * c->W32 * 4ull)) != cudaSuccess) return oom(e, "slab allocation");
   if (getenv("REI_TRACE")) {
     cudaStreamSynchronize(c->stream);
     fprintf(stderr, "[rei_alloc] arena %llu entries: %.3f ms\n", (unsigned long long)new_cap,
@@ -327,6 +346,7 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
     CUDA_OK(c, cudaMemcpyAsync(t, c->tarena, keep_slabs * 32ull * c->W32 * 4ull, cudaMemcpyDeviceToDevice,
                                c->stream));
   CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  const uint64_t old_cap = c->cap, old_slots = c->slots;
   c->dfree(c->arena); c->dfree(c->bp); c->dfree(c->tarena);
   c->arena = a; c->bp = b; c->tarena = t;
   c->cap = new_cap;
@@ -335,9 +355,20 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
     uint64_t want = 1;
     while (want < 2 * new_cap) want <<= 1;
     if (want != c->slots) {
+      // the table's contents are rebuilt from the arena after a growth: release first
       c->dfree(c->table);
       c->table = nullptr;
-      CUDA_OK(c, c->dmalloc(&c->table, want * 8ull));
+      e = c->dmalloc(&c->table, want * slot_bytes(c));
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        c->err = std::string("dedup table allocation: ") + cudaGetErrorString(e);
+        if (old_slots && c->dmalloc(&c->table, old_slots * slot_bytes(c)) == cudaSuccess) {
+          c->cap = std::min(old_cap, new_cap);  // entries the previous table was sized for
+          return REI_OUT_OF_MEMORY;
+        }
+        c->slots = 0;
+        return REI_ECUDA;
+      }
       c->slots = want;
     }
   }
@@ -373,7 +404,7 @@ rei_status clear_dedup(Ctx* c) {
   if (c->mode == DEDUP_BITMAP) {
     CUDA_OK(c, cudaMemsetAsync(c->bitmap, 0, c->bitmap_words * 4, c->stream));
   } else {
-    CUDA_OK(c, cudaMemsetAsync(c->table, c->mode == DEDUP_HASH64 ? 0xff : 0x00, c->slots * 8, c->stream));
+    CUDA_OK(c, cudaMemsetAsync(c->table, c->mode == DEDUP_HASHIDX ? 0x00 : 0xff, c->slots * slot_bytes(c), c->stream));
     CUDA_OK(c, cudaMemsetAsync(c->special, 0, sizeof(unsigned int), c->stream));
   }
   return REI_OK;
@@ -609,19 +640,33 @@ rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
   return REI_OK;
 }
 
-// Device memory the context may use: rei_options.mem_budget_bytes, else 80 % of the
-// free HBM (plus the allocator's idle blocks), queried lazily: cudaMemGetInfo costs
-// 0.3-70 ms per call on B200 (measured), so a bitmap-mode context whose fixed-size
-// cache is small never asks.
+// Device memory the context's cache may use: rei_options.mem_budget_bytes (a fixed total),
+// else 80 % of the free HBM as the process-wide pool estimates it (dev_free_estimate:
+// one cudaMemGetInfo per process -- 0.3-70 ms on B200 -- then the pool's own traffic).
+// Sharded-cache contexts allocate outside the pool and query the driver once.
 uint64_t budget_of(Ctx* c) {
-  if (!c->budget) {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    if (!c->sharded) fr += dev_pool_idle_bytes(c->device);  // idle blocks the allocator keeps
-    c->budget = (uint64_t)(0.8 * (double)fr);
-    c->budget = c->budget > c->budget_used ? c->budget - c->budget_used : 0;
+  if (c->budget_user) return c->budget;
+  if (c->sharded) {
+    if (!c->budget) {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      c->budget = (uint64_t)(0.8 * (double)fr);
+    }
+    return c->budget;
   }
-  return c->budget;
+  return (uint64_t)(0.8 * (double)dev_free_estimate(c->device));
+}
+
+// Bytes of the cache buffers for `cap` entries: arena + back-pointers + transposed
+// slabs (abt) and the dedup table (power-of-two slots, load <= 1/2).
+uint64_t abt_bytes(const Ctx* c, uint64_t cap) {
+  return cap * (4ull * c->W32 + 8ull) + (cap / 32 + 4096) * 32ull * c->W32 * 4ull;
+}
+uint64_t table_bytes(const Ctx* c, uint64_t cap) {
+  if (c->mode == DEDUP_BITMAP) return 0;
+  uint64_t want = 1;
+  while (want < 2 * cap) want <<= 1;
+  return want * slot_bytes(c);
 }
 
 // Total HBM of the current device, queried once per process and device.
@@ -638,17 +683,40 @@ uint64_t device_total_bytes(int dev) {
 
 rei_status grow(Ctx* c, uint64_t need_entries) {
   if (c->sharded) return REI_OUT_OF_MEMORY;  // peers map the buffers: fixed at rei_init
-  uint64_t max_cap = budget_of(c) / bytes_per_entry(c);
-  if (c->entry_limit) max_cap = std::min<uint64_t>(max_cap, c->entry_limit);
-  if (c->cap >= max_cap) return REI_OUT_OF_MEMORY;
+  // the bitmap-mode cache already holds every one of the 2^n possible CSs: nothing to
+  // grow, and no cudaMemGetInfo (0.3-70 ms on B200) for the budget (it was the 8-15 ms
+  // tail of fresh-context solves of Table 1 row 1 at level 28)
+  if (c->mode == DEDUP_BITMAP && c->cap >= (1ull << c->tab.n) + 64) return REI_OUT_OF_MEMORY;
+  if (c->entry_limit && c->cap >= c->entry_limit) return REI_OUT_OF_MEMORY;
   // x8 per growth: every growth rehashes the whole cache, so grow rarely
   uint64_t nc = std::max<uint64_t>(c->cap * 8, need_entries);
   if (c->mode == DEDUP_BITMAP) nc = std::min<uint64_t>(nc, (1ull << c->tab.n) + 64);
-  nc = std::min(nc, max_cap);
+  if (c->entry_limit) nc = std::min<uint64_t>(nc, c->entry_limit);
+  // memory: with a user budget the new buffers must fit it; otherwise the new arena /
+  // back-pointer / slab buffers must fit next to the old ones (they are copied), and the
+  // new buffers with the new table must fit once the old ones are released
+  const uint64_t B = budget_of(c), held = abt_bytes(c, c->cap) + table_bytes(c, c->cap);
+  auto fits = [&](uint64_t cap) {
+    if (c->budget_user) return abt_bytes(c, cap) + table_bytes(c, cap) <= B;
+    return abt_bytes(c, cap) <= B && abt_bytes(c, cap) + table_bytes(c, cap) <= B + held;
+  };
+  if (!fits(nc)) {  // the largest capacity in (cap, nc) that fits
+    uint64_t lo = c->cap, hi = nc;
+    while (hi - lo > 1) {
+      const uint64_t mid = lo + (hi - lo) / 2;
+      (fits(mid) ? lo : hi) = mid;
+    }
+    nc = lo;
+  }
   if (nc <= c->cap) return REI_OUT_OF_MEMORY;
   const bool trace = getenv("REI_TRACE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   rei_status s = alloc_arena(c, nc, c->arena_used, c->slabs_used);
+  if (s == REI_OUT_OF_MEMORY && c->mode != DEDUP_BITMAP && c->table) {
+    // the previous buffers are in place (the table may have been re-allocated empty)
+    rei_status r = rebuild_dedup(c, c->arena_used);
+    return r != REI_OK ? r : s;
+  }
   if (s != REI_OK) return s;
   const auto t1 = std::chrono::steady_clock::now();
   s = rebuild_dedup(c, c->arena_used);
@@ -1001,6 +1069,19 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   for (const Block& b : cat) catv[b.slice_a ? 1 : 0].push_back(b);
   for (auto& v : catv) renumber_items(v);
   const std::vector<Block>* lists[3] = {&catv[0], &catv[1], &uni};
+  {
+    // the pair kernels stage a launch's block table in shared memory next to <= 64 KB
+    // of split tables and append stages: refuse a level whose table cannot fit
+    static int optin = 0;
+    if (!optin && cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device) != cudaSuccess)
+      optin = 227 * 1024;
+    for (int r = 0; r < 3; ++r)
+      if (lists[r]->size() * sizeof(Block) + 64 * 1024 > (size_t)optin) {
+        c->err = "level " + std::to_string(cost) + " has " + std::to_string(lists[r]->size()) +
+                 " operand blocks in one launch; their table exceeds the shared memory of a CTA";
+        return REI_EINVAL;
+      }
+  }
   for (int r = 0; r < 3; ++r) {
     if (lists[r]->empty()) continue;
     std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
@@ -1028,6 +1109,12 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   cudaStream_t su = conc >= 1 ? c->aux[0] : c->stream;
   cudaStream_t sn = conc >= 2 ? c->aux[1] : c->stream;
   cudaStream_t sc = conc >= 3 ? c->aux[2] : c->stream;
+  if ((c->concurrency == 5 || c->concurrency == 6) && conc >= 3) {
+    // union on the context's stream (no event wait: it reaches the SMs first), concat on
+    // an auxiliary stream: the persistent union grid runs ahead of concat, whose CTAs
+    // fill the SMs as union CTAs retire (an early exit at c* is met in union first)
+    sn = c->stream;
+  }
   if (conc >= 1) {
     CUDA_OK(c, cudaEventRecord(c->ev_fork, c->stream));
     for (int i = 0; i < conc; ++i) CUDA_OK(c, cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0));
@@ -1601,6 +1688,19 @@ rei_status launch_sharded(Ctx* c, int rank, int world, const std::vector<UnaryWo
   for (const Block& b : cat) catv[b.slice_a ? 1 : 0].push_back(b);
   for (auto& v : catv) renumber_items(v);
   const std::vector<Block>* lists[3] = {&catv[0], &catv[1], &uni};
+  {
+    // the pair kernels stage a launch's block table in shared memory next to <= 64 KB
+    // of split tables and append stages: refuse a level whose table cannot fit
+    static int optin = 0;
+    if (!optin && cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device) != cudaSuccess)
+      optin = 227 * 1024;
+    for (int r = 0; r < 3; ++r)
+      if (lists[r]->size() * sizeof(Block) + 64 * 1024 > (size_t)optin) {
+        c->err = "a sharded level has " + std::to_string(lists[r]->size()) +
+                 " operand blocks in one launch; their table exceeds the shared memory of a CTA";
+        return REI_EINVAL;
+      }
+  }
   for (int r = 0; r < 3; ++r) {
     if (lists[r]->empty()) continue;
     std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
@@ -1954,6 +2054,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     c->err_den = opts->err_den ? opts->err_den : 1;
     c->flags = opts->flags;
     c->budget = opts->mem_budget_bytes;
+    c->budget_user = opts->mem_budget_bytes != 0;
     c->entry_limit = opts->max_entries;
     c->sharded = (opts->flags & REI_FLAG_SHARDED_CACHE) != 0;
     c->allgather = opts->allgather;
@@ -2042,6 +2143,11 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   c->d2h_bytes += 64 + 8ull * c->tab.n;  // table summary + IC keys
   c->W32 = next_pow2_words(c->tab.n);
   c->mode = (c->tab.n <= 32) ? DEDUP_BITMAP : (c->W32 == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
+  // wide CSs whose top bits are free keep the whole CS in the slot (one sector per probe,
+  // no arena read on a fingerprint match); REI_INDEXED_KEYS=1 keeps fingerprint + index
+  if (c->mode == DEDUP_HASHIDX && ((c->W32 == 4 && c->tab.n <= 127) || (c->W32 == 8 && c->tab.n <= 254)) &&
+      getenv("REI_INDEXED_KEYS") == nullptr)
+    c->mode = DEDUP_HASHIN;
   // Finished levels are reordered by the top 12 bits of their bitmap position (A/B on
   // B200, full final level: Table 1 row 1 67.5 -> 63.6 ms, row 8 neutral; a full 25-bit
   // sort cut the kernels as much but cost more).  REI_NO_LEVEL_SORT disables it.
@@ -2066,12 +2172,12 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     // the HBM hash sets (two-word C2: 253 -> 212 ms -- the DRAM-bound kernels interfere
     // less when concat has priority).
     const char* ev = getenv("REI_CONCURRENT");
-    c->concurrency = ev ? std::max(0, std::min(4, atoi(ev))) : (c->mode == DEDUP_BITMAP ? 2 : 3);
+    c->concurrency = ev ? std::max(0, std::min(6, atoi(ev))) : (c->mode == DEDUP_BITMAP ? 2 : 3);
     const int nstreams = std::min(3, c->concurrency);
     if (nstreams >= 1) {
       int prio_lo = 0, prio_hi = 0;
       cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-      const int low = c->concurrency == 3 ? 1 : c->concurrency == 4 ? 2 : -1;
+      const int low = c->concurrency == 3 ? 1 : (c->concurrency == 4 || c->concurrency == 6) ? 2 : -1;
       for (int i = 0; i < nstreams; ++i)
         if (cudaStreamCreateWithPriority(&c->aux[i], cudaStreamNonBlocking, i == low ? prio_lo : prio_hi) !=
                 cudaSuccess ||
@@ -2085,15 +2191,14 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   if (c->mode == DEDUP_BITMAP) {
     c->bitmap_words = std::max<uint64_t>(1, (1ull << c->tab.n) / 32);
     if (c->dmalloc(&c->bitmap, c->bitmap_words * 4) != cudaSuccess) return fail("bitmap allocation failed");
-    if (c->budget) c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
-    else c->budget_used = c->bitmap_words * 4;  // charged when the budget is first queried
+    if (c->budget_user) c->budget = c->budget > c->bitmap_words * 4 ? c->budget - c->bitmap_words * 4 : 0;
   }
   // bitmap mode: at most 2^n distinct CSs exist, so reserve them all up front (up to
   // 2^28 entries); hash modes start at 2^22 entries and grow ahead of each level.
   uint64_t cap0 = 1ull << 22;
   if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(1ull << 28, (1ull << c->tab.n) + 64);
   // the free-memory query is skipped when the initial cache is < 1/8 of the HBM
-  if (c->budget || c->sharded || cap0 * bytes_per_entry(c.get()) > device_total_bytes(c->device) / 8)
+  if (c->budget_user || c->sharded || cap0 * bytes_per_entry(c.get()) > device_total_bytes(c->device) / 8)
     cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, budget_of(c.get()) / bytes_per_entry(c.get())));
   phase("budget");
   if (c->sharded) {  // sized once: peers map these buffers, so they never move

@@ -49,13 +49,16 @@ struct LevelCtl {
   unsigned long long pad[2];
 };
 
-enum DedupMode : int { DEDUP_BITMAP = 0, DEDUP_HASH64 = 1, DEDUP_HASHIDX = 2 };
+// DEDUP_HASHIN: the CS itself is the slot (16 B for W32 = 4, 32 B for W32 = 8), so a
+// probe that hits costs one random 32-byte sector; used when the top CS bit(s) are
+// never set (|IC| <= 127 / 254), which frees the all-ones pattern as the empty slot.
+enum DedupMode : int { DEDUP_BITMAP = 0, DEDUP_HASH64 = 1, DEDUP_HASHIDX = 2, DEDUP_HASHIN = 3 };
 
 struct Dedup {
   int mode;
   int pad;
   uint32_t* bitmap;                 // DEDUP_BITMAP: 2^n bits
-  unsigned long long* table;        // DEDUP_HASH64 / DEDUP_HASHIDX
+  unsigned long long* table;        // DEDUP_HASH64 / DEDUP_HASHIDX / DEDUP_HASHIN (W32 / 2 u64 per slot)
   unsigned long long mask;          // slots - 1
   unsigned int* special;            // DEDUP_HASH64: persistent "all-ones key present" flag
 };

@@ -80,6 +80,10 @@ int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const u
 cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st);
 void dev_free(void* p, cudaStream_t st);
 uint64_t dev_pool_idle_bytes(int dev);
+// Free device memory as this process sees it: one cudaMemGetInfo per device, then the
+// pool's own cudaMalloc / cudaFree traffic, plus its idle blocks (releasable on demand).
+uint64_t dev_free_estimate(int dev);
+void dev_free_estimate_reset(int dev);  // re-query on the next estimate (after an OOM)
 cudaError_t host_alloc(void** p, size_t bytes);
 void host_free(void* p);
 void release_cached_memory();

@@ -153,17 +153,55 @@ def test_search_parity_wide(sp, K):
     compare_search(sp, K)
 
 
+@pytest.mark.parametrize("sp,K", W4 + W8, ids=ids(W4 + W8))
+def test_indexed_keys_parity(sp, K, monkeypatch):
+    # the fingerprint + arena-index hash set (REI_INDEXED_KEYS; the default for |IC| in
+    # 65..127 / 129..254 keeps the whole CS in the slot) reaches the same level sets
+    monkeypatch.setenv("REI_INDEXED_KEYS", "1")
+    compare_search(sp, K)
+
+
+@pytest.mark.parametrize("sp", [W4[1][0], W8[0][0]], ids=["w4", "w8"])
+def test_inline_keys_growth(sp):
+    # a small first cache forces growths of the inline-key table (rehash of every entry)
+    o = oracle.Oracle.from_spec(sp)
+    ro = o.solve(12)
+    rg = gpu_solver(sp, mem_budget_bytes=48 << 20).solve(12)
+    assert rg.status in (ro.status, "out_of_memory")
+    if rg.status == ro.status:
+        assert rg.cost == ro.cost
+    want = {l.cost: l.unique for l in ro.levels}
+    got = {l.cost: l.unique for l in rg.levels if l.complete == 1}
+    assert got and all(got[c] == want[c] for c in got)
+
+
+def test_ic_over_512_is_einval_and_device_stays_usable():
+    # |IC| > 512 (a binary string of length 57 has ~1.6k infixes) is rejected at rei_init
+    # without touching out-of-bounds shared memory; the CUDA context stays usable
+    from paper_2305_18575_b200 import ReiError
+    rng = random.Random(3)
+    long_word = "".join(rng.choice("01") for _ in range(57))
+    with pytest.raises(ReiError):
+        gpu_solver(specgen.Spec("01", (long_word,), ("0",)))
+    sp, K = SMALL[1]
+    ro = oracle.Oracle.from_spec(sp).solve(K)
+    rg = gpu_solver(sp).solve(K)
+    assert (rg.status, rg.cost) == (ro.status, ro.cost)
+
+
 @pytest.mark.parametrize("var", ["REI_GENERIC_CONCAT", "REI_GENERIC_UNARY"])
-@pytest.mark.parametrize("sp,K", RANDOM_W1[:3] + W2[:2], ids=ids(RANDOM_W1[:3] + W2[:2]))
+@pytest.mark.parametrize("sp,K", RANDOM_W1[:3] + W2[:2] + W4[:1] + W8[:1],
+                         ids=ids(RANDOM_W1[:3] + W2[:2] + W4[:1] + W8[:1]))
 def test_generic_kernels_parity(sp, K, var, monkeypatch):
     # the generic (any split count) concat / unary kernels, used when a word has > 15
-    # proper splits, exercised on one- and two-word CSs too
+    # proper splits, exercised on one- and two-word CSs too; on wide CSs the generic
+    # unary kernel is the per-thread star (the default is the sliced k_unary_wide)
     monkeypatch.setenv(var, "1")
     compare_search(sp, K)
 
 
 @pytest.mark.parametrize("order", ["0", "1"])
-@pytest.mark.parametrize("conc", ["0", "2", "3"])
+@pytest.mark.parametrize("conc", ["0", "2", "3", "5"])
 @pytest.mark.parametrize("sp,K", RANDOM_W1[:2] + W2[:1], ids=ids(RANDOM_W1[:2] + W2[:1]))
 def test_launch_order_and_streams_parity(sp, K, order, conc, monkeypatch):
     # a level's kernels are independent (REI_UNION_FIRST = launch order, REI_CONCURRENT =
@@ -178,6 +216,14 @@ def test_launch_order_and_streams_parity(sp, K, order, conc, monkeypatch):
     assert (rg.status, rg.cost) == (ro.status, ro.cost)
     if ro.status == "found" and rg.regex not in ("empty", "eps"):
         assert precise(rg.regex, sp.P, sp.N)
+
+
+@pytest.mark.parametrize("waves", ["4", "64"])
+@pytest.mark.parametrize("sp,K", RANDOM_W1[:2] + W2[:1], ids=ids(RANDOM_W1[:2] + W2[:1]))
+def test_concat_waves_parity(sp, K, waves, monkeypatch):
+    # concat grids of several waves of CTAs (REI_CONCAT_WAVES) cover the same work items
+    monkeypatch.setenv("REI_CONCAT_WAVES", waves)
+    compare_search(sp, K)
 
 
 @pytest.mark.parametrize("sp", [specgen.Spec("01", ("0" * 20, "1"), ("0" * 19, "11")),
