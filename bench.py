@@ -62,6 +62,12 @@ WORKLOADS = {
     "c4-planted-s0": (specgen.gen_planted("abcd", "(a+b+c)*d(a+c)(b+d)", 10, 10, 4, 8, 0), 40,
                       "BASELINE configs[3]: planted 4-symbol target, |IC|=148 (256-bit CS), unit costs (c*=16), "
                       "5e8 candidates"),
+    "c3-big": (specgen.gen_planted("01", "(0+1)*0(0+1)(0+1)(0+1)(0+1)", 10, 10, 6, 10, 2, costs=(20, 20, 20, 5, 30)),
+               800, "BASELINE configs[2] at throughput scale: planted binary target, |IC|=103 (128-bit CS), costs "
+                    "(20,20,20,5,30) (P:1356 style), c*=375, 1.45e10 candidates, 1.7e9 cached CSs"),
+    "c4-big": (specgen.gen_planted("abcd", "(a+b+c)*d(a+c)(b+d)", 10, 10, 6, 10, 1, costs=(20, 20, 20, 5, 30)),
+               800, "BASELINE configs[3] at throughput scale: planted 4-symbol target, |IC|=188 (256-bit CS), costs "
+                    "(20,20,20,5,30), c*=315, 1.26e10 candidates, 8e8 cached CSs"),
     "c2-t2-s4": (specgen.gen_type2("01", 6, 10, 10, 4), 40,
                  "BASELINE configs[1]: Type 2 (P:1244-1253) binary, le=6, p=n=10, seed 4 "
                  "(|IC|=48, c*=25, ~2.7e10 candidates, 1.5e9 cached CSs)"),
@@ -74,10 +80,12 @@ PAPER = {
                     "hw": "Colab A100-SXM4-40GB (P:1147-1153)"},
 }
 ORACLE_SAMPLE_COST = {"table1-row1": 18, "table1-row8": 150, "c1-toy": 8, "c2-t1-s0": 16, "c2-t1-s3": 16,
-                      "c2-t2-s4": 16, "c3-planted-s1": 13, "c3-planted-s1-nu": 245, "c4-planted-s0": 11}
+                      "c2-t2-s4": 16, "c3-planted-s1": 13, "c3-planted-s1-nu": 245, "c4-planted-s0": 11,
+                      "c3-big": 245, "c4-big": 230}
 # cpu_baseline sample
 REFERENCE_STEP_COST = {"table1-row1": 16, "table1-row8": 140, "c1-toy": 8, "c2-t1-s0": 14, "c2-t1-s3": 14,
-                       "c2-t2-s4": 14, "c3-planted-s1": 12, "c3-planted-s1-nu": 230, "c4-planted-s0": 10}
+                       "c2-t2-s4": 14, "c3-planted-s1": 12, "c3-planted-s1-nu": 230, "c4-planted-s0": 10,
+                       "c3-big": 230, "c4-big": 215}
 # --impl reference step
 
 METRIC = "candidate REs/sec"
@@ -247,14 +255,14 @@ def run_reference(args, rank):
 
 # ------------------------------------------------------------------ our arm
 
-def roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, workload):
+def roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, workload, mode="hash64"):
     """Dominant kernel's achieved rate vs its binding ceiling."""
     dom = max(("concat", "union", "unary", "transpose"), key=lambda k: kstats[k][1])
     dom_launches, dom_ms = kstats[dom]
     evaluated = 0
     for rr in kresults:
         for l in rr.levels:
-            evaluated += {"concat": l.eval_c, "union": l.eval_u}.get(dom, l.evaluated)
+            evaluated += {"concat": l.eval_c, "union": l.eval_u}.get(dom, l.cand_q + l.cand_s)
     s_in = sum(max(0, len(w) - 1) for w in ic_words)
     peaks, peaks_kind = load_peaks()
     ip = load_int_peaks()
@@ -285,7 +293,9 @@ def roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, w
         # fingerprint match when keys are indexed (W32 >= 4).  Bound: the measured rate
         # of random 32-byte reads from a table >> L2 (scripts/microbench/peaks.cu);
         # the copy-bandwidth fraction is given beside it.
-        sectors = 1 if w32 == 2 else 1 + (4 * w32 + 31) // 32
+        # inline keys (hash64, 16/32-byte inline slots): the slot is the key -> one sector;
+        # indexed keys: the 8-byte slot plus the arena CS on a fingerprint match
+        sectors = 1 if mode in ("hash64", "inline") else 1 + (4 * w32 + 31) // 32
         bps = 32 * sectors
         rnd = ip["random_reads_per_s"] or 36.3e9
         hbm_peak = float(peaks.get("hbm_gbs", 6650.0)) * 1e9
@@ -357,6 +367,7 @@ def measure(args, workload, rank, world, local_rank, stream, flush, sharded, ste
     launches = solver.launch_count() - launches0
     kstats_timed = solver.kernel_stats()
     ic_words = solver.ic()
+    mode = solver.dedup_mode()
     solver.close()  # the kernel pass and the e2e solves below run one context at a time
     dev = torch.device("cuda", local_rank)
     total_ms, all_cands = reduce_over_ranks(sum(step_ms), cands, dev, world, sum_work=not sharded)
@@ -374,7 +385,7 @@ def measure(args, workload, rank, world, local_rank, stream, flush, sharded, ste
     # L2 flushed) -- the launch order ncu serialises too.  Concat goes first there
     # (REI_UNION_FIRST=0): with union first on one stream, a union hit at c* makes the
     # concat launches of that level exit at once.
-    roof_timed = roofline_of(kstats_timed, results, step_ms, ic_words, w32, world, "timed region", workload)
+    roof_timed = roofline_of(kstats_timed, results, step_ms, ic_words, w32, world, "timed region", workload, mode)
     kresults, kstep_ms, kstats, kernel_pass = results, step_ms, kstats_timed, "timed region"
     if world == 1:
         prev = {k: os.environ.get(k) for k in ("REI_CONCURRENT", "REI_UNION_FIRST")}
@@ -406,7 +417,7 @@ def measure(args, workload, rank, world, local_rank, stream, flush, sharded, ste
         kstats = ksolver.kernel_stats()
         ksolver.close()
         kernel_pass = f"sequential-stream pass (REI_CONCURRENT=0, REI_UNION_FIRST=0), {steps} steps, L2 flushed"
-    roofline = roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, workload)
+    roofline = roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, workload, mode)
     roofline["frac_timed_region"] = roof_timed["frac"]
     roofline["kernel_timed_region"] = roof_timed["kernel"]
 
@@ -460,7 +471,7 @@ def measure(args, workload, rank, world, local_rank, stream, flush, sharded, ste
                                     "(CUDA events per level)"},
         "config": {
             "workload": workload, "description": desc, "max_cost": max_cost,
-            "n_ic": r0.n_ic, "cs_bits": 32 * r0.cs_words, "cstar": r0.cost, "regex": r0.regex,
+            "n_ic": r0.n_ic, "cs_bits": 32 * r0.cs_words, "dedup": mode, "cstar": r0.cost, "regex": r0.regex,
             "candidates_per_step": cands / steps,
             "candidates_through_last_complete_level": r0.cand_complete,
             "time_to_minimal_re_ms": statistics.median(step_ms),

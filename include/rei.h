@@ -156,6 +156,11 @@ rei_status rei_kernel_stats(const void* ctx, rei_kernel_class k, uint64_t* launc
 rei_status rei_reset_kernel_stats(void* ctx);
 /* Total kernel launches issued by this context (all classes). */
 uint64_t rei_launch_count(const void* ctx);
+/* The dedup set rei_init chose for this specification:
+ * 0 = bitmap over all 2^|IC| CSs (|IC| <= 32), 1 = 8-byte inline keys (|IC| <= 64),
+ * 2 = 32-bit fingerprint + arena index per 8-byte slot, 3 = the whole CS inline in a
+ * 16- or 32-byte slot (|IC| 65..127 and 129..254).  -1 for a NULL context. */
+int rei_dedup_mode(const void* ctx);
 /* Host<->device bytes copied by this context since creation (inputs, level plans,
  * control lines, results). */
 rei_status rei_transfer_bytes(const void* ctx, uint64_t* h2d, uint64_t* d2h);

@@ -376,7 +376,28 @@ struct WarpStage {
   uint32_t* cs;               // [kStage][W] (shared)
   unsigned long long* rank;   // [kStage] (shared)
   uint32_t n;                 // entries held (warp-uniform)
+  unsigned long long* lc = nullptr;  // [kLocal] keys known to be in the dedup set (shared)
 };
+
+// Per-warp cache of 64-bit keys known to be in the HBM hash set (DEDUP_HASH64): the set
+// only grows during a search, so a key found here is a duplicate for certain and its
+// global probe (one random HBM sector) is skipped -- exact, like the operand-equality
+// filter.  Direct-mapped by hash bits 20.. (the slot uses the low bits).  A warp's
+// candidates share a uniform operand across slabs, and x.y repeats along a row
+// (40-60 % within-row duplicates).  REI_LOCAL_CACHE = entries (0 = off).
+#ifndef REI_LOCAL_CACHE
+#define REI_LOCAL_CACHE 0
+#endif
+constexpr int kLocal = REI_LOCAL_CACHE;
+template <int W>
+__device__ __forceinline__ void stage_init_lc(WarpStage<W>& st, unsigned long long* base) {
+  if (kLocal == 0 || W != 2) return;
+  st.lc = base + (threadIdx.x >> 5) * kLocal;
+  for (int i = threadIdx.x & 31; i < kLocal; i += 32) st.lc[i] = ~0ull;
+  __syncwarp();
+}
+// shared bytes of the local caches of one CTA of `warps` warps
+constexpr size_t local_cache_bytes(int W, int warps) { return (kLocal && W == 2) ? (size_t)warps * kLocal * 8 : 0; }
 
 // Out of line: the flush is rare and must not bloat the probe loop's instruction stream.
 template <int W>
@@ -558,21 +579,41 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
       }
       if (!stage) return;
     } else {
-      unsigned long long slot[G], val[G], key[G];
+      unsigned long long slot[G], val[G], key[G], hh[G];
+      bool need[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
-        const bool need = valid[g] && !skip[g];
+        need[g] = valid[g] && !skip[g];
         key[g] = key64<W>(cs[g]);
-        slot[g] = hash_cs<W>(cs[g]) & p.dedup.mask;
-        val[g] = need ? p.dedup.table[slot[g]] : key[g];
+        hh[g] = hash_cs<W>(cs[g]);
+        slot[g] = hh[g] & p.dedup.mask;
       }
+#ifdef REI_WARP_MATCH
+      // equal keys within a group of 32 candidates: only the lowest lane probes
+      if (stage) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const unsigned m = __match_any_sync(kFull, key[g]) & __ballot_sync(kFull, need[g]);
+          if (need[g] && (threadIdx.x & 31) != (uint32_t)(__ffs(m) - 1)) need[g] = false;
+        }
+      }
+#endif
+      uint32_t lci[G];
+      if (kLocal && stage && stage->lc) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          lci[g] = (uint32_t)(hh[g] >> 20) & (uint32_t)(kLocal - 1);
+          if (need[g] && key[g] != kEmpty64 && stage->lc[lci[g]] == key[g]) need[g] = false;
+        }
+      }
+#pragma unroll
+      for (int g = 0; g < G; ++g) val[g] = need[g] ? p.dedup.table[slot[g]] : key[g];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         isnew[g] = false;
-        if (val[g] != key[g] || key[g] == kEmpty64) {
-          const bool need = valid[g] && !skip[g];
-          isnew[g] = need && insert_hash64(p, key[g], slot[g], val[g]);
-        }
+        if (val[g] != key[g] || key[g] == kEmpty64) isnew[g] = need[g] && insert_hash64(p, key[g], slot[g], val[g]);
+        // the key is in the set now (found or inserted): remember it
+        if (kLocal && stage && stage->lc && need[g] && key[g] != kEmpty64) stage->lc[lci[g]] = key[g];
       }
     }
     // precision on the new CSs, then append
@@ -974,6 +1015,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
     stage.cs = st_cs + warp * kStage * W;
     stage.rank = st_rank + warp * kStage;
     stage.n = 0;
+    stage_init_lc<W>(stage, st_rank + kWarps * kStage);
   }
   // split masks: bit of the uniform operand that enables split k of word q*32+lane
   uint32_t mlo[W][MAXK], mhi[W][MAXK];
@@ -1201,6 +1243,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 
     stage.cs = st_cs + warp * kStage * W;
     stage.rank = st_rank + warp * kStage;
     stage.n = 0;
+    if (W <= 2) stage_init_lc<W>(stage, st_rank + kWarps * kStage);
   }
 
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
@@ -1377,6 +1420,7 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
     stage.cs = st_cs + warp * kStage * W;
     stage.rank = st_rank + warp * kStage;
     stage.n = 0;
+    stage_init_lc<W>(stage, st_rank + 8 * kStage);
   }
   constexpr int NW = 32 * W;
   const uint32_t lane = lane_id();
@@ -1752,7 +1796,7 @@ template <int W, int MAXK, bool SA>
 int launch_concat_fast_t(const LevelParams& p, cudaStream_t st) {
   // (one-word CSs append directly: no per-warp stage, more of the SM's L1 for probes)
   const size_t smem = p.nblocks * sizeof(Block) + (size_t)MAXK * 32 * W * 4 +
-                      (W == 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
+                      (W == 2 ? (size_t)kWarps * kStage * (W * 4 + 8) + local_cache_bytes(W, kWarps) : 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_concat_fast<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 #ifdef REI_CARVEOUT
@@ -1796,7 +1840,8 @@ int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
 
 template <int W, bool SH>
 int launch_union_sh(const LevelParams& p, cudaStream_t st) {
-  const size_t smem = p.nblocks * sizeof(Block) + (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) : 0);
+  const size_t smem = p.nblocks * sizeof(Block) +
+                      (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) + local_cache_bytes(W, kWarps) : 0);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_union<W, SH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 #ifdef REI_CARVEOUT
@@ -1816,7 +1861,9 @@ template <int W, int MAXK>
 int launch_unary_fast_t(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
                         unsigned long long bq, unsigned long long bs, unsigned long long slab_s, cudaStream_t st) {
   const unsigned long long slabs = (n_q + 31) / 32 + (n_s + 31) / 32;
-  const size_t smem = (size_t)8 * kStage * (W * 4 + 8);
+  const size_t smem = (size_t)8 * kStage * (W * 4 + 8) + local_cache_bytes(W, 8);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_unary_fast<W, MAXK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_for(k_unary_fast<W, MAXK>, 256, smem, 8, slabs);
   k_unary_fast<W, MAXK><<<grid, 256, smem, st>>>(p, n_q, n_s, bq, bs, slab_s);
   return 1;

@@ -138,6 +138,7 @@ struct Ctx {
   uint64_t bitmap_words = 0;
   unsigned long long* table = nullptr;
   uint64_t slots = 0;
+  uint64_t table_slot_bytes = 0;  // slot size the dedup table was allocated with
   unsigned int* special = nullptr;
   LevelCtl* ctl = nullptr;       // the current level's control line (in ctl_base)
   LevelCtl* ctl_base = nullptr;  // [2]: sharded mode alternates by level parity
@@ -354,7 +355,7 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
   if (c->mode != DEDUP_BITMAP) {
     uint64_t want = 1;
     while (want < 2 * new_cap) want <<= 1;
-    if (want != c->slots) {
+    if (want != c->slots || c->table_slot_bytes != slot_bytes(c)) {
       // the table's contents are rebuilt from the arena after a growth: release first
       c->dfree(c->table);
       c->table = nullptr;
@@ -362,7 +363,8 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
       if (e != cudaSuccess) {
         cudaGetLastError();
         c->err = std::string("dedup table allocation: ") + cudaGetErrorString(e);
-        if (old_slots && c->dmalloc(&c->table, old_slots * slot_bytes(c)) == cudaSuccess) {
+        if (old_slots && c->table_slot_bytes == slot_bytes(c) &&
+            c->dmalloc(&c->table, old_slots * slot_bytes(c)) == cudaSuccess) {
           c->cap = std::min(old_cap, new_cap);  // entries the previous table was sized for
           return REI_OUT_OF_MEMORY;
         }
@@ -370,6 +372,7 @@ rei_status alloc_arena(Ctx* c, uint64_t new_cap, uint64_t keep, uint64_t keep_sl
         return REI_ECUDA;
       }
       c->slots = want;
+      c->table_slot_bytes = slot_bytes(c);
     }
   }
   return REI_OK;
@@ -700,6 +703,13 @@ rei_status grow(Ctx* c, uint64_t need_entries) {
     if (c->budget_user) return abt_bytes(c, cap) + table_bytes(c, cap) <= B;
     return abt_bytes(c, cap) <= B && abt_bytes(c, cap) + table_bytes(c, cap) <= B + held;
   };
+  if (!fits(nc) && c->mode == DEDUP_HASHIN) {
+    // inline wide keys cost 2 x 16-32 bytes of table per entry: when they no longer fit,
+    // continue with fingerprint + index slots (8 bytes; the table is rebuilt from the
+    // arena after every growth anyway, so the switch costs nothing extra)
+    c->mode = DEDUP_HASHIDX;
+    if (!fits(nc)) c->mode = DEDUP_HASHIN;
+  }
   if (!fits(nc)) {  // the largest capacity in (cap, nc) that fits
     uint64_t lo = c->cap, hi = nc;
     while (hi - lo > 1) {
@@ -712,6 +722,7 @@ rei_status grow(Ctx* c, uint64_t need_entries) {
   const bool trace = getenv("REI_TRACE") != nullptr;
   const auto t0 = std::chrono::steady_clock::now();
   rei_status s = alloc_arena(c, nc, c->arena_used, c->slabs_used);
+  if (s != REI_OK && c->table && c->table_slot_bytes != slot_bytes(c)) c->mode = DEDUP_HASHIN;  // switch undone
   if (s == REI_OUT_OF_MEMORY && c->mode != DEDUP_BITMAP && c->table) {
     // the previous buffers are in place (the table may have been re-allocated empty)
     rei_status r = rebuild_dedup(c, c->arena_used);
@@ -2266,6 +2277,8 @@ rei_status rei_reset_kernel_stats(void* ctx) {
 }
 
 uint64_t rei_launch_count(const void* ctx) { return ctx ? static_cast<const Ctx*>(ctx)->launches : 0; }
+
+int rei_dedup_mode(const void* ctx) { return ctx ? static_cast<const Ctx*>(ctx)->mode : -1; }
 
 rei_status rei_transfer_bytes(const void* ctx, uint64_t* h2d, uint64_t* d2h) {
   if (!ctx) return REI_EINVAL;

@@ -124,6 +124,8 @@ def load_library():
     lib.rei_reset_kernel_stats.argtypes = [vp]
     lib.rei_launch_count.restype = c.c_uint64
     lib.rei_launch_count.argtypes = [vp]
+    lib.rei_dedup_mode.restype = c.c_int
+    lib.rei_dedup_mode.argtypes = [vp]
     lib.rei_transfer_bytes.restype = c.c_int
     lib.rei_transfer_bytes.argtypes = [vp, c.POINTER(c.c_uint64), c.POINTER(c.c_uint64)]
     lib.rei_last_error.restype = c.c_char_p
@@ -317,6 +319,12 @@ class Solver:
 
     def launch_count(self) -> int:
         return int(self._lib.rei_launch_count(self._h))
+
+    DEDUP_MODES = ("bitmap", "hash64", "indexed", "inline")
+
+    def dedup_mode(self) -> str:
+        """The dedup set rei_init chose (include/rei.h rei_dedup_mode)."""
+        return self.DEDUP_MODES[self._lib.rei_dedup_mode(self._h)]
 
     def transfer_bytes(self) -> Tuple[int, int]:
         h, d = ctypes.c_uint64(), ctypes.c_uint64()

@@ -249,8 +249,28 @@ int main2() {
   return 0;
 }
 
+// One random 8-byte-read pass over the largest table (for an ncu capture of the DRAM
+// bytes one random read really moves).
+int main3() {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, 0));
+  g_sms = prop.multiProcessorCount;
+  size_t freeb, totalb;
+  CK(cudaMemGetInfo(&freeb, &totalb));
+  size_t maxb = 16ull << 30;
+  while (maxb > freeb * 8 / 10) maxb >>= 1;
+  unsigned long long* tab;
+  CK(cudaMalloc(&tab, maxb));
+  k_fill<<<g_sms * 8, 256>>>(tab, maxb / 8);
+  CK(cudaDeviceSynchronize());
+  run_gather2<8, 0>("random_read_cv", tab, maxb, maxb);
+  CK(cudaFree(tab));
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && argv[1][0] == '2') return main2();
+  if (argc > 1 && argv[1][0] == '3') return main3();
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
   g_sms = prop.multiProcessorCount;
