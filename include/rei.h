@@ -63,6 +63,10 @@ typedef struct {
                                             once at rei_init (no growth); G ranks hold G x the
                                             entries of one.  Needs world_size > 1 with `allgather`
                                             (one process per rank) or rei_solve_group.          */
+#define REI_FLAG_SMALL_CACHE 8u          /* start the language cache at 2^16 entries and grow
+                                            x8 on demand, also in bitmap mode (which otherwise
+                                            reserves all 2^|IC| entries at rei_init): many
+                                            small contexts alive at once (f4)              */
 
 /* Host all-gather supplied by the caller for REI_FLAG_SHARDED_CACHE across processes
  * (the binding builds it on torch.distributed): every rank passes `bytes` bytes in
@@ -246,6 +250,17 @@ rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_resu
  * result and status (the call returns REI_OK once every context was attempted). */
 rei_status rei_solve_batch(void* const* ctxs, size_t n, uint32_t max_cost, int threads, rei_result* out,
                            rei_status* status);
+/* Packed solve of n contexts on ONE device (the paper's suites of many
+ * small runs): all specifications advance one non-empty cost level per
+ * step, and each step runs every kernel class (?/*, union, concatenation of either
+ * orientation, per CS width and split-count class) as one launch whose CTA groups
+ * serve the specifications, with one control-line gather and one sync per step.
+ * Same arithmetic and results as rei_solve.  Contexts with |IC| > 64,
+ * words of more than 16 symbols, a level overflow or a multi-GPU / sharded setup
+ * are solved alone after the packed steps.  out[i] / status[i] as rei_solve;
+ * done_seconds[i] (may be NULL) = host seconds from the call to context i's result. */
+rei_status rei_solve_packed(void* const* ctxs, size_t n, uint32_t max_cost, rei_result* out, rei_status* status,
+                            double* done_seconds);
 
 /* ---- multi-GPU host logic (pure functions, usable without a GPU) ---- */
 

@@ -5,7 +5,7 @@ binding.  ``build`` compiles the library in-tree.  There is no CPU fallback.
 """
 from .rei import (LevelStat, ReiError, Result, Solver, cs_owner, exchange_offsets, load_library,  # noqa: F401
                   nccl_unique_id,
-                  partition, release_cached_memory, solve, solve_batch, solve_group)
+                  partition, release_cached_memory, solve, solve_batch, solve_group, solve_packed)
 
-__all__ = ["Solver", "Result", "LevelStat", "ReiError", "solve", "solve_batch", "solve_group",
+__all__ = ["Solver", "Result", "LevelStat", "ReiError", "solve", "solve_batch", "solve_group", "solve_packed",
            "nccl_unique_id", "partition", "load_library", "release_cached_memory"]

@@ -313,12 +313,17 @@ __device__ bool insert_inline(const S& p, const unsigned long long (&k)[W / 2], 
     }
     if (v0 == k[0] && (v1 & ~(W == 8 ? kPend : 0ull)) == k[1]) {
       if (W == 4) return false;
-      while (v1 & kPend) {  // the owner is writing the low half
+      // a low half equal to the key's is the key, whatever order the loads took (a slot
+      // only ever goes from empty to its final value): the common hit needs no fence
+      unsigned long long w0, w1;
+      ld16v(slot + 2, w0, w1);
+      if (w0 == k[U > 2 ? 2 : 0] && w1 == k[U > 2 ? 3 : 1]) return false;
+      // otherwise wait until the owner has published its low half, then read it in order
+      while (v1 & kPend) {
         __nanosleep(20);
         v1 = *(volatile unsigned long long*)(slot + 1);
       }
       __threadfence();
-      unsigned long long w0, w1;
       ld16v(slot + 2, w0, w1);
       if (w0 == k[U > 2 ? 2 : 0] && w1 == k[U > 2 ? 3 : 1]) return false;
     }
@@ -792,6 +797,30 @@ __device__ __forceinline__ int find_block(const Block* blocks, int nb, unsigned 
   return lo;
 }
 
+// Packed launches: this CTA's specification (binary search of its group), its
+// parameters copied to shared memory, and its block index / count within the group.
+__device__ __forceinline__ const LevelParams& packed_params(const Packed& pk, uint32_t& bid, uint32_t& nbid) {
+  __shared__ LevelParams s_p;
+  __shared__ uint32_t s_i;
+  if (threadIdx.x == 0) {
+    uint32_t lo = 0, hi = pk.nspec - 1;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi + 1) >> 1;
+      if (pk.cta_start[mid] <= blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    s_i = lo;
+  }
+  __syncthreads();
+  const uint32_t i = s_i;
+  const uint32_t* src = reinterpret_cast<const uint32_t*>(pk.params + i);
+  uint32_t* dst = reinterpret_cast<uint32_t*>(&s_p);
+  for (uint32_t k = threadIdx.x; k < sizeof(LevelParams) / 4; k += blockDim.x) dst[k] = src[k];
+  bid = blockIdx.x - pk.cta_start[i];
+  nbid = pk.cta_start[i + 1] - pk.cta_start[i];
+  __syncthreads();
+  return s_p;
+}
+
 __device__ __forceinline__ bool found_and_stop(const LevelParams& p) {
   return p.early_exit && *(volatile unsigned long long*)&p.ctl->found_rank != ~0ull;
 }
@@ -960,7 +989,7 @@ template <int W, int MAXK, bool SLICE_A>
 #ifndef REI_CONCAT_MINB1
 #define REI_CONCAT_MINB1 3
 #endif
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_concat_fast(LevelParams p) {
+__device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t bid, uint32_t nbid) {
   static_assert(W <= 2, "fast path is for one- and two-word CSs");
   constexpr int NW = 32 * W;
 #ifndef REI_CONCAT_G1
@@ -1042,8 +1071,8 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
 #endif
     }
   }
-  const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+  const unsigned long long gwarp = (unsigned long long)bid * kWarps + (threadIdx.x >> 5);
+  const unsigned long long nwarps = (unsigned long long)nbid * kWarps;
 
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
@@ -1214,6 +1243,17 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_
   if (W == 2) stage_flush<W>(p, stage);
 }
 
+template <int W, int MAXK, bool SLICE_A>
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_concat_fast(LevelParams p) {
+  concat_fast_body<W, MAXK, SLICE_A>(p, blockIdx.x, gridDim.x);
+}
+template <int W, int MAXK, bool SLICE_A>
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_concat_fast_packed(Packed pk) {
+  uint32_t bid, nbid;
+  const LevelParams& p = packed_params(pk, bid, nbid);
+  concat_fast_body<W, MAXK, SLICE_A>(p, bid, nbid);
+}
+
 // ============================================================================
 // Union kernel: uniform operand x, lane t holds operand_t of the sliced level.
 template <int W, bool SH = false>
@@ -1225,15 +1265,15 @@ template <int W, bool SH = false>
 #ifndef REI_UNION_G1
 #define REI_UNION_G1 4
 #endif
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : 1)) k_union(LevelParams p) {  // (minB: W = 2 keeps 2 CTAs per SM)
+__device__ __forceinline__ void union_body(const LevelParams& p, uint32_t bid, uint32_t nbid) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
   __syncthreads();
   const uint32_t lane = lane_id();
-  const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + (threadIdx.x >> 5);
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+  const unsigned long long gwarp = (unsigned long long)bid * kWarps + (threadIdx.x >> 5);
+  const unsigned long long nwarps = (unsigned long long)nbid * kWarps;
   constexpr int G = W == 1 ? REI_UNION_G1 : Batch<W>::G;
   WarpStage<W> stage;  // (W <= 2) new CSs staged per warp after the block table
   {
@@ -1336,6 +1376,18 @@ __global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 
   if (kUnionStaged && W <= 2) stage_flush<W>(p, stage);
 }
 
+// (minB: W = 2 keeps 2 CTAs per SM)
+template <int W, bool SH = false>
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : 1)) k_union(LevelParams p) {
+  union_body<W, SH>(p, blockIdx.x, gridDim.x);
+}
+template <int W>
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : 1)) k_union_packed(Packed pk) {
+  uint32_t bid, nbid;
+  const LevelParams& p = packed_params(pk, bid, nbid);
+  union_body<W, false>(p, bid, nbid);
+}
+
 // ============================================================================
 // Unary kernel: thread per operand; first n_q are question marks (x | eps),
 // the rest stars: single shortlex pass  s[eps] = 1,
@@ -1407,9 +1459,9 @@ __global__ void __launch_bounds__(256) k_unary(LevelParams p, unsigned long long
 // shuffling X[u] and S[v] from their lanes; a transpose turns the 32 slices into the
 // 32 operands' stars (same fixpoint as star_cs).
 template <int W, int MAXK>
-__global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned long long n_q, unsigned long long n_s,
-                                                    unsigned long long base_q, unsigned long long base_s,
-                                                    unsigned long long slab_s) {
+__device__ __forceinline__ void unary_fast_body(const LevelParams& p, unsigned long long n_q, unsigned long long n_s,
+                                                unsigned long long base_q, unsigned long long base_s,
+                                                unsigned long long slab_s, uint32_t bid, uint32_t nbid) {
   static_assert(W <= 2, "sliced unary kernel is for one- and two-word CSs");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   WarpStage<W> stage;  // new CSs staged per warp: [8 warps][kStage][W] + ranks
@@ -1443,8 +1495,8 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
   const unsigned long long tb = p.item_begin;  // this rank's operand share [tb, te)
   const unsigned long long te = total < (unsigned long long)p.total_items ? total : (unsigned long long)p.total_items;
   const unsigned long long slabs_q = (n_q + 31) / 32, slabs_s = (n_s + 31) / 32;
-  const unsigned long long gwarp = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned long long gwarp = ((unsigned long long)bid * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nwarps = ((unsigned long long)nbid * blockDim.x) >> 5;
   uint32_t evaluated = 0;
   constexpr int G = 4;  // slabs per batch: G independent probes per lane in flight
   const unsigned long long nslab = slabs_q + slabs_s;
@@ -1534,6 +1586,21 @@ __global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned l
   stage_flush<W>(p, stage);
   const uint32_t tot = __reduce_add_sync(kFull, evaluated);
   if (lane == 0 && tot) atomicAdd(&p.ctl->evaluated, (unsigned long long)tot);
+}
+
+template <int W, int MAXK>
+__global__ void __launch_bounds__(256, 2) k_unary_fast(LevelParams p, unsigned long long n_q, unsigned long long n_s,
+                                                    unsigned long long base_q, unsigned long long base_s,
+                                                    unsigned long long slab_s) {
+  unary_fast_body<W, MAXK>(p, n_q, n_s, base_q, base_s, slab_s, blockIdx.x, gridDim.x);
+}
+// packed: the ? / * operand counts and bases travel in the spec's LevelParams
+// (rank_base = 0, unary_* fields)
+template <int W, int MAXK>
+__global__ void __launch_bounds__(256, 2) k_unary_fast_packed(Packed pk) {
+  uint32_t bid, nbid;
+  const LevelParams& p = packed_params(pk, bid, nbid);
+  unary_fast_body<W, MAXK>(p, p.un_q, p.un_s, p.un_bq, p.un_bs, p.un_slab, bid, nbid);
 }
 
 // Bit-sliced unary kernel for wide CSs (W32 >= 4, |IC| > 64): a warp takes a slab of
@@ -1644,13 +1711,14 @@ __global__ void k_seeds(LevelParams p, const uint32_t* seeds, int nsym) {
 
 // Level c -> transposed slabs: warp per slab, T[32q + w] bit t = CS_t[32q + w].
 template <int W>
-__global__ void k_transpose(const uint32_t* __restrict__ arena, unsigned long long base, unsigned long long count,
-                            uint32_t* __restrict__ tarena, unsigned long long slab_base) {
+__device__ __forceinline__ void transpose_body(const uint32_t* __restrict__ arena, unsigned long long base,
+                                               unsigned long long count, uint32_t* __restrict__ tarena,
+                                               unsigned long long slab_base, uint32_t bid, uint32_t nbid) {
   constexpr int NW = 32 * W;
   const uint32_t lane = lane_id();
   const unsigned long long nslabs = (count + 31) / 32;
-  const unsigned long long gw = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  const unsigned long long gw = ((unsigned long long)bid * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nw = ((unsigned long long)nbid * blockDim.x) >> 5;
   for (unsigned long long s = gw; s < nslabs; s += nw) {
     const unsigned long long e = s * 32 + lane;
     uint32_t x[W];
@@ -1662,6 +1730,19 @@ __global__ void k_transpose(const uint32_t* __restrict__ arena, unsigned long lo
 #pragma unroll
     for (int q = 0; q < W; ++q) tarena[(slab_base + s) * NW + q * 32 + lane] = transpose32(x[q], lane);
   }
+}
+
+template <int W>
+__global__ void k_transpose(const uint32_t* __restrict__ arena, unsigned long long base, unsigned long long count,
+                            uint32_t* __restrict__ tarena, unsigned long long slab_base) {
+  transpose_body<W>(arena, base, count, tarena, slab_base, blockIdx.x, gridDim.x);
+}
+// packed: spec i transposes its level [un_bq, un_bq + un_q) into slabs from un_slab
+template <int W>
+__global__ void k_transpose_packed(Packed pk) {
+  uint32_t bid, nbid;
+  const LevelParams& p = packed_params(pk, bid, nbid);
+  transpose_body<W>(p.arena, p.un_bq, p.un_q, const_cast<uint32_t*>(p.tarena), p.un_slab, bid, nbid);
 }
 
 // (Re)insert arena entries [base, base + count) into the dedup set (after growth, or
@@ -1915,7 +1996,99 @@ int launch_ops_t(const LevelParams& p, int op, const uint32_t* a, const uint32_t
   return 1;
 }
 
+// ---- packed launches (f4): one grid serves many specifications (CTA groups)
+__global__ void k_ctl_reset_packed(const LevelParams* __restrict__ params, uint32_t n) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    LevelCtl* c = params[i].ctl;
+    c->found_rank = ~0ull;
+    c->count = 0;
+    c->evaluated = 0;
+    c->overflow = 0;
+    c->special_seen = 0;
+    c->eval_c = 0;
+    c->eval_u = 0;
+  }
+}
+__global__ void k_ctl_gather_packed(const LevelParams* __restrict__ params, uint32_t n, LevelCtl* __restrict__ out) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = *params[i].ctl;
+}
+
+template <int W, int MAXK, bool SA>
+int launch_concat_packed_t(const Packed& pk, uint32_t ctas, size_t nblocks_max, cudaStream_t st) {
+  const size_t smem = nblocks_max * sizeof(Block) + (size_t)MAXK * 32 * W * 4 +
+                      (W == 2 ? (size_t)kWarps * kStage * (W * 4 + 8) + local_cache_bytes(W, kWarps) : 0);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_concat_fast_packed<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_concat_fast_packed<W, MAXK, SA><<<ctas, kWarps * 32, smem, st>>>(pk);
+  return 1;
+}
+template <int W, bool SA>
+int launch_concat_packed_k(int maxk, const Packed& pk, uint32_t ctas, size_t nb, cudaStream_t st) {
+  if (maxk <= 1) return launch_concat_packed_t<W, 1, SA>(pk, ctas, nb, st);
+  if (maxk <= 3) return launch_concat_packed_t<W, 3, SA>(pk, ctas, nb, st);
+  if (maxk <= 7) return launch_concat_packed_t<W, 7, SA>(pk, ctas, nb, st);
+  return launch_concat_packed_t<W, 15, SA>(pk, ctas, nb, st);
+}
+template <int W>
+int launch_union_packed_t(const Packed& pk, uint32_t ctas, size_t nblocks_max, cudaStream_t st) {
+  const size_t smem = nblocks_max * sizeof(Block) +
+                      (W <= 2 ? (size_t)kWarps * kStage * (W * 4 + 8) + local_cache_bytes(W, kWarps) : 0);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_union_packed<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_union_packed<W><<<ctas, kWarps * 32, smem, st>>>(pk);
+  return 1;
+}
+template <int W, int MAXK>
+int launch_unary_packed_t(const Packed& pk, uint32_t ctas, cudaStream_t st) {
+  const size_t smem = (size_t)8 * kStage * (W * 4 + 8) + local_cache_bytes(W, 8);
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_unary_fast_packed<W, MAXK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_unary_fast_packed<W, MAXK><<<ctas, 256, smem, st>>>(pk);
+  return 1;
+}
+
 }  // namespace
+
+int packable(int W32, int maxk) { return (W32 == 1 || W32 == 2) && maxk <= 15 ? 1 : 0; }
+int maxk_class(int maxk) { return maxk <= 1 ? 1 : maxk <= 3 ? 3 : maxk <= 7 ? 7 : 15; }
+
+int launch_ctl_reset_packed(const LevelParams* params, uint32_t n, cudaStream_t st) {
+  k_ctl_reset_packed<<<std::max(1u, std::min(64u, (n + 255) / 256)), 256, 0, st>>>(params, n);
+  return 1;
+}
+int launch_ctl_gather_packed(const LevelParams* params, uint32_t n, LevelCtl* out, cudaStream_t st) {
+  k_ctl_gather_packed<<<std::max(1u, std::min(64u, (n + 255) / 256)), 256, 0, st>>>(params, n, out);
+  return 1;
+}
+int launch_concat_packed(int W32, int maxk, bool slice_a, const Packed& pk, uint32_t ctas, size_t nb, cudaStream_t st) {
+  if (W32 == 1) return slice_a ? launch_concat_packed_k<1, true>(maxk, pk, ctas, nb, st)
+                               : launch_concat_packed_k<1, false>(maxk, pk, ctas, nb, st);
+  if (W32 == 2) return slice_a ? launch_concat_packed_k<2, true>(maxk, pk, ctas, nb, st)
+                               : launch_concat_packed_k<2, false>(maxk, pk, ctas, nb, st);
+  return 0;
+}
+int launch_union_packed(int W32, const Packed& pk, uint32_t ctas, size_t nb, cudaStream_t st) {
+  if (W32 == 1) return launch_union_packed_t<1>(pk, ctas, nb, st);
+  if (W32 == 2) return launch_union_packed_t<2>(pk, ctas, nb, st);
+  return 0;
+}
+int launch_unary_packed(int W32, int maxk, const Packed& pk, uint32_t ctas, cudaStream_t st) {
+  auto go = [&](auto w) {
+    constexpr int W = decltype(w)::value;
+    if (maxk <= 1) return launch_unary_packed_t<W, 1>(pk, ctas, st);
+    if (maxk <= 3) return launch_unary_packed_t<W, 3>(pk, ctas, st);
+    if (maxk <= 7) return launch_unary_packed_t<W, 7>(pk, ctas, st);
+    return launch_unary_packed_t<W, 15>(pk, ctas, st);
+  };
+  if (W32 == 1) return go(std::integral_constant<int, 1>{});
+  if (W32 == 2) return go(std::integral_constant<int, 2>{});
+  return 0;
+}
+int launch_transpose_packed(int W32, const Packed& pk, uint32_t ctas, cudaStream_t st) {
+  if (W32 == 1) { k_transpose_packed<1><<<ctas, 256, 0, st>>>(pk); return 1; }
+  if (W32 == 2) { k_transpose_packed<2><<<ctas, 256, 0, st>>>(pk); return 1; }
+  return 0;
+}
 
 #define REI_DISPATCH_W(W32, ...)                 \
   switch (W32) {                                 \

@@ -1992,6 +1992,379 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
   return solve_group(g, max_cost);
 }
 
+// ============================================================================
+// Many small specifications in packed launches (the paper's suites
+// of thousands of small runs).  Every active specification advances one
+// non-empty cost level per step; a step runs each kernel class (?/*, union, concat of
+// either orientation; per CS width and split-count class) as ONE launch whose CTA
+// groups serve the specifications (Packed / packed_params in levels.cu), resets and
+// gathers all control lines with one kernel each, and syncs once.  The arithmetic is
+// the single-spec kernels' (same bodies).  A specification that needs anything else
+// (wider CSs, > 15 proper splits, a level overflow, OnTheFly) leaves the packed loop
+// and is solved alone afterwards.
+struct PackSpec {
+  Ctx* c = nullptr;
+  int cost = 0;
+  uint64_t cand = 1;
+  bool active = false, fallback = false;
+  rei_status st = REI_OK;
+  LevelInfo lv;
+  std::vector<Block> cat, uni, catv[2];
+  uint64_t nq = 0, ns = 0, ncat = 0, nuni = 0;
+  double done_s = 0;  // host seconds from the start of the call to this spec's result
+};
+
+struct PackBuf {  // device + pinned staging of one step
+  LevelParams* d_params = nullptr;
+  LevelParams* h_params = nullptr;
+  uint32_t* d_cta = nullptr;
+  uint32_t* h_cta = nullptr;
+  Block* d_blocks = nullptr;
+  Block* h_blocks = nullptr;
+  LevelCtl* d_ctl = nullptr;
+  LevelCtl* h_ctl = nullptr;
+  size_t cap_params = 0, cap_cta = 0, cap_blocks = 0, cap_ctl = 0;
+  ~PackBuf() {
+    for (void* q : {(void*)d_params, (void*)d_cta, (void*)d_blocks, (void*)d_ctl}) if (q) cudaFree(q);
+    for (void* q : {(void*)h_params, (void*)h_cta, (void*)h_blocks, (void*)h_ctl}) if (q) cudaFreeHost(q);
+  }
+  template <class T>
+  static bool ensure(T*& d, T*& h, size_t& cap, size_t n) {
+    if (n <= cap) return true;
+    const size_t c2 = std::max<size_t>(n, 2 * cap);
+    if (d) cudaFree(d);
+    if (h) cudaFreeHost(h);
+    d = nullptr; h = nullptr; cap = 0;
+    if (cudaMalloc(&d, c2 * sizeof(T)) != cudaSuccess || cudaMallocHost(&h, c2 * sizeof(T)) != cudaSuccess) return false;
+    cap = c2;
+    return true;
+  }
+};
+
+rei_status solve_packed(std::vector<Ctx*>& cs, uint32_t max_cost, std::vector<rei_status>& status,
+                        std::vector<double>& done_s, const std::vector<cudaStream_t>& own_streams) {
+  const size_t n = cs.size();
+  const auto t0 = std::chrono::steady_clock::now();
+  auto now_s = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+  cudaStream_t st = cs[0]->stream;
+  std::vector<PackSpec> sp(n);
+  status.assign(n, REI_OK);
+  done_s.assign(n, 0.0);
+  PackBuf pb;
+  rei_status s;
+  // ---- level c1 (Alg. 1 line 3) and the trivial answers (lines 1-2), per spec
+  for (size_t i = 0; i < n; ++i) {
+    Ctx* c = cs[i];
+    PackSpec& q = sp[i];
+    q.c = c;
+    reset_search(c);
+    c->sort_levels = false;  // a level's order is free; packed steps skip the sort
+    const rei_costs& k = c->costs;
+    const uint64_t total_ex = c->P.size() + c->N.size();
+    const bool empty_ok = c->P.empty() ||
+                          (c->err_num && (uint64_t)c->P.size() * c->err_den <= (uint64_t)c->err_num * total_ex);
+    const bool eps_ok = c->P.size() == 1 && c->P[0].empty();
+    if (empty_ok || eps_ok) {
+      c->regex = empty_ok ? "empty" : "eps";
+      c->result.cost = k.sym;
+      c->result.candidates = 1;
+      continue;
+    }
+    if (c->tab.n == 0 || c->world > 1 || c->sharded || !packable(c->W32, c->tab.maxk) || c->otf_level) {
+      q.fallback = true;
+      continue;
+    }
+    if ((s = clear_dedup(c)) != REI_OK || (s = reset_ctl(c)) != REI_OK) return s;
+    LevelParams p;
+    fill_params(c, p);
+    p.out_base = 0;
+    c->launches += launch_seeds(c->W32, p, c->tab.seeds, (int)c->alphabet.size(), st);
+    q.active = true;
+  }
+  CUDA_OK(cs[0], cudaGetLastError());
+  for (size_t i = 0; i < n; ++i)
+    if (sp[i].active)
+      CUDA_OK(sp[i].c, cudaMemcpyAsync(sp[i].c->h_ctl, sp[i].c->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, st));
+  CUDA_OK(cs[0], cudaStreamSynchronize(st));
+  for (size_t i = 0; i < n; ++i) {
+    PackSpec& q = sp[i];
+    if (!q.active) continue;
+    Ctx* c = q.c;
+    const int c1 = (int)c->costs.sym;
+    LevelInfo lv;
+    lv.cost = c1;
+    lv.seeds = true;
+    lv.size = c->h_ctl->count;
+    c->levels[c1] = lv;
+    c->arena_used = lv.size;
+    rei_level_stat stt{};
+    stt.cost = c1;
+    stt.unique = lv.size;
+    const uint64_t found_seed = c->h_ctl->found_rank;
+    stt.complete = found_seed == ~0ull ? 1 : 0;
+    c->stats.push_back(stt);
+    if (found_seed != ~0ull) {
+      c->result.candidates = 1 + found_seed + 1;
+      if ((status[i] = finish_found(c, c1, found_seed)) != REI_OK) {}
+      q.active = false;
+      done_s[i] = now_s();
+      continue;
+    }
+    q.cand = 1 + c->alphabet.size();
+    q.cost = c1;
+    c->launches += launch_transpose(c->W32, c->arena, 0, c->arena_used, c->tarena, 0, st);
+    c->slabs_used = (c->arena_used + 31) / 32;
+    c->result.last_complete_cost = c1;
+    c->result.cand_complete = q.cand;
+    c->result.candidates = q.cand;
+  }
+
+  struct Item { uint32_t spec; uint64_t work; LevelParams p; };
+  for (;;) {
+    // ---- plan: every active spec's next non-empty level
+    std::vector<size_t> act;
+    for (size_t i = 0; i < n; ++i) {
+      PackSpec& q = sp[i];
+      if (!q.active) continue;
+      Ctx* c = q.c;
+      const rei_costs& k = c->costs;
+      bool planned = false;
+      while (q.cost < (int)max_cost) {
+        ++q.cost;
+        q.lv = LevelInfo{};
+        q.lv.cost = q.cost;
+        plan_level(c, q.cost, q.lv, q.cat, q.uni, q.nq, q.ns, q.ncat, q.nuni);
+        if (!q.lv.plan.empty()) { planned = true; break; }
+      }
+      if (!planned) {
+        status[i] = REI_NOT_FOUND;
+        q.active = false;
+        done_s[i] = now_s();
+        continue;
+      }
+      if ((int)(q.cat.size() + q.uni.size()) > Ctx::kMaxBlocks) { q.active = false; q.fallback = true; continue; }
+      const uint64_t prev = c->stats.empty() ? 0 : c->stats.back().unique;
+      const uint64_t expect = std::min<uint64_t>(q.nq + q.ns + q.ncat + q.nuni, 4 * prev + 1024);
+      if (c->arena_used + expect > c->cap || c->slabs_used + expect / 32 + 2 > c->slab_cap) {
+        if ((s = grow(c, c->arena_used + expect)) != REI_OK && s != REI_OUT_OF_MEMORY) return s;
+      }
+      q.lv.begin = c->arena_used;
+      q.lv.slab = c->slabs_used;
+      q.catv[0].clear();
+      q.catv[1].clear();
+      for (const Block& b : q.cat) q.catv[b.slice_a ? 1 : 0].push_back(b);
+      for (auto& v : q.catv) renumber_items(v);
+      act.push_back(i);
+    }
+    if (act.empty()) break;
+    const auto step_t0 = std::chrono::steady_clock::now();
+    // ---- work classes: (kind, W32, maxk class, orientation) -> items of the specs
+    std::map<std::tuple<int, int, int, int>, std::vector<Item>> cls;
+    std::vector<Block> blocks;
+    std::vector<LevelParams> ctlp;  // one LevelParams per active spec (control-line reset / gather)
+    std::vector<std::pair<size_t, size_t>> boff;  // (item list ref) -> block offset, patched below
+    struct Patch { std::tuple<int, int, int, int> key; size_t idx; size_t off; };
+    std::vector<Patch> patches;
+    for (size_t a = 0; a < act.size(); ++a) {
+      PackSpec& q = sp[act[a]];
+      Ctx* c = q.c;
+      const rei_costs& k = c->costs;
+      LevelParams p;
+      fill_params(c, p);
+      p.out_base = q.lv.begin;
+      ctlp.push_back(p);
+      const int mk = maxk_class(c->tab.maxk);
+      if (q.nq + q.ns) {
+        LevelParams pu = p;
+        pu.item_begin = 0;
+        pu.total_items = q.nq + q.ns;
+        pu.un_q = q.nq;
+        pu.un_s = q.ns;
+        pu.un_bq = q.nq ? c->levels.at(q.cost - (int)k.opt).begin : 0;
+        pu.un_bs = q.ns ? c->levels.at(q.cost - (int)k.star).begin : 0;
+        pu.un_slab = q.ns ? c->levels.at(q.cost - (int)k.star).slab : 0;
+        cls[{0, c->W32, mk, 0}].push_back({(uint32_t)a, (q.nq + 31) / 32 + (q.ns + 31) / 32, pu});
+      }
+      auto add_pairs = [&](int kind, int orient, const std::vector<Block>& v) {
+        if (v.empty()) return;
+        LevelParams pc = p;
+        pc.nblocks = (uint32_t)v.size();
+        pc.item_begin = 0;
+        pc.total_items = items_of(v);
+        auto key = std::make_tuple(kind, c->W32, kind == 1 ? mk : 0, orient);
+        patches.push_back({key, cls[key].size(), blocks.size()});
+        blocks.insert(blocks.end(), v.begin(), v.end());
+        cls[key].push_back({(uint32_t)a, pc.total_items, pc});
+      };
+      add_pairs(2, 0, q.uni);      // union
+      add_pairs(1, 0, q.catv[0]);  // concat, uniform left operand
+      add_pairs(1, 1, q.catv[1]);  // concat, sliced left operand
+    }
+    // ---- one upload: control params, every class's params and CTA groups, block tables
+    size_t np = ctlp.size(), ncta = 0;
+    for (auto& kv : cls) { np += kv.second.size(); ncta += kv.second.size() + 1; }
+    if (!PackBuf::ensure(pb.d_params, pb.h_params, pb.cap_params, np) ||
+        !PackBuf::ensure(pb.d_cta, pb.h_cta, pb.cap_cta, std::max<size_t>(1, ncta)) ||
+        !PackBuf::ensure(pb.d_blocks, pb.h_blocks, pb.cap_blocks, std::max<size_t>(1, blocks.size())) ||
+        !PackBuf::ensure(pb.d_ctl, pb.h_ctl, pb.cap_ctl, act.size())) {
+      cs[0]->err = "packed staging allocation failed";
+      return REI_OUT_OF_MEMORY;
+    }
+    for (auto& pt : patches) cls[pt.key][pt.idx].p.blocks = pb.d_blocks + pt.off;
+    std::copy(blocks.begin(), blocks.end(), pb.h_blocks);
+    std::copy(ctlp.begin(), ctlp.end(), pb.h_params);
+    size_t po = ctlp.size(), co = 0;
+    struct Launch { std::tuple<int, int, int, int> key; size_t params, cta, nspec; uint32_t ctas; size_t maxnb; };
+    std::vector<Launch> launches;
+    const uint32_t budget = 148u * 4u * 4u;  // CTAs per packed launch: ~4 resident per SM x 4 waves
+    for (auto& kv : cls) {
+      auto& items = kv.second;
+      uint64_t tot = 0;
+      size_t maxnb = 0;
+      for (auto& it : items) { tot += it.work; maxnb = std::max<size_t>(maxnb, it.p.nblocks); }
+      uint32_t* cta = pb.h_cta + co;
+      uint32_t acc = 0;
+      for (size_t j = 0; j < items.size(); ++j) {
+        cta[j] = acc;
+        const uint64_t per = std::get<0>(kv.first) == 0 ? 8 : 8;  // work units per CTA (warps)
+        uint64_t want = std::max<uint64_t>(1, (items[j].work + per - 1) / per);
+        const uint64_t share = std::max<uint64_t>(1, tot ? (uint64_t)((double)budget * items[j].work / tot) : 1);
+        acc += (uint32_t)std::min(want, share);
+        pb.h_params[po + j] = items[j].p;
+      }
+      cta[items.size()] = acc;
+      launches.push_back({kv.first, po, co, items.size(), acc, maxnb});
+      po += items.size();
+      co += items.size() + 1;
+    }
+    Ctx* c0 = cs[0];
+    CUDA_OK(c0, cudaMemcpyAsync(pb.d_blocks, pb.h_blocks, std::max<size_t>(1, blocks.size()) * sizeof(Block),
+                                cudaMemcpyHostToDevice, st));
+    CUDA_OK(c0, cudaMemcpyAsync(pb.d_params, pb.h_params, po * sizeof(LevelParams), cudaMemcpyHostToDevice, st));
+    CUDA_OK(c0, cudaMemcpyAsync(pb.d_cta, pb.h_cta, std::max<size_t>(1, co) * sizeof(uint32_t),
+                                cudaMemcpyHostToDevice, st));
+    uint64_t nl = launch_ctl_reset_packed(pb.d_params, (uint32_t)ctlp.size(), st);
+    // unary, union, then concat (union first: a precise union stops the concat CTAs)
+    for (int kind : {0, 2, 1}) {
+      for (auto& L : launches) {
+        if (std::get<0>(L.key) != kind) continue;
+        Packed pk{pb.d_params + L.params, pb.d_cta + L.cta, (uint32_t)L.nspec};
+        const int W = std::get<1>(L.key), mk = std::get<2>(L.key);
+        if (kind == 0) nl += launch_unary_packed(W, mk, pk, L.ctas, st);
+        else if (kind == 2) nl += launch_union_packed(W, pk, L.ctas, L.maxnb, st);
+        else nl += launch_concat_packed(W, mk, std::get<3>(L.key) == 1, pk, L.ctas, L.maxnb, st);
+      }
+    }
+    nl += launch_ctl_gather_packed(pb.d_params, (uint32_t)ctlp.size(), pb.d_ctl, st);
+    CUDA_OK(c0, cudaGetLastError());
+    CUDA_OK(c0, cudaMemcpyAsync(pb.h_ctl, pb.d_ctl, act.size() * sizeof(LevelCtl), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(c0, cudaStreamSynchronize(st));
+    c0->launches += nl;
+    const double step_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - step_t0).count();
+    // ---- per spec: found / overflow / next level; transposes of the new levels (packed)
+    std::vector<LevelParams> tp;
+    std::map<int, std::vector<LevelParams>> tpw;
+    for (size_t a = 0; a < act.size(); ++a) {
+      const size_t i = act[a];
+      PackSpec& q = sp[i];
+      Ctx* c = q.c;
+      const LevelCtl& l = pb.h_ctl[a];
+      if (l.overflow) {  // redo this spec alone (grows its cache, OnTheFly if needed)
+        q.active = false;
+        q.fallback = true;
+        continue;
+      }
+      rei_level_stat stt{};
+      stt.cost = (uint32_t)q.cost;
+      stt.cand_q = q.nq; stt.cand_s = q.ns; stt.cand_c = q.ncat; stt.cand_u = q.nuni;
+      stt.ms = step_ms;
+      const bool found = l.found_rank != ~0ull;
+      const bool complete = !found || (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
+      stt.unique = l.count;
+      stt.complete = complete ? 1 : 0;
+      stt.evaluated = complete ? (q.nq + q.ns + q.ncat + q.nuni) : l.evaluated;
+      stt.eval_c = complete ? q.ncat : l.eval_c;
+      stt.eval_u = complete ? q.nuni : l.eval_u;
+      q.lv.size = l.count;
+      c->arena_used = q.lv.begin + q.lv.size;
+      c->levels[q.cost] = q.lv;
+      c->stats.push_back(stt);
+      if (found) {
+        c->result.candidates = q.cand + stt.evaluated;
+        if (complete) {
+          c->result.last_complete_cost = (uint32_t)q.cost;
+          c->result.cand_complete = q.cand + stt.evaluated;
+        }
+        status[i] = finish_found(c, q.cost, l.found_rank);
+        q.active = false;
+        done_s[i] = now_s();
+        continue;
+      }
+      q.cand += q.nq + q.ns + q.ncat + q.nuni;
+      c->result.cand_complete = q.cand;
+      c->result.candidates = q.cand;
+      c->result.last_complete_cost = (uint32_t)q.cost;
+      if (c->slabs_used + (q.lv.size + 31) / 32 > c->slab_cap) {
+        if ((s = grow(c, c->cap + 1)) != REI_OK) { q.active = false; q.fallback = true; continue; }
+      }
+      LevelParams p;
+      fill_params(c, p);
+      p.un_q = q.lv.size;
+      p.un_bq = q.lv.begin;
+      p.un_slab = q.lv.slab;
+      tpw[c->W32].push_back(p);
+      c->slabs_used += (q.lv.size + 31) / 32;
+    }
+    // packed transposes: one launch per CS width
+    size_t tpo = 0, tco = 0, tn = 0;
+    for (auto& kv : tpw) tn += kv.second.size();
+    if (tn) {
+      if (!PackBuf::ensure(pb.d_params, pb.h_params, pb.cap_params, tn) ||
+          !PackBuf::ensure(pb.d_cta, pb.h_cta, pb.cap_cta, tn + tpw.size())) {
+        cs[0]->err = "packed staging allocation failed";
+        return REI_OUT_OF_MEMORY;
+      }
+      std::vector<std::tuple<int, size_t, size_t, size_t, uint32_t>> tl;
+      for (auto& kv : tpw) {
+        uint32_t acc = 0;
+        for (size_t j = 0; j < kv.second.size(); ++j) {
+          pb.h_cta[tco + j] = acc;
+          acc += (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(64, (kv.second[j].un_q + 255) / 256));
+          pb.h_params[tpo + j] = kv.second[j];
+        }
+        pb.h_cta[tco + kv.second.size()] = acc;
+        tl.emplace_back(kv.first, tpo, tco, kv.second.size(), acc);
+        tpo += kv.second.size();
+        tco += kv.second.size() + 1;
+      }
+      CUDA_OK(c0, cudaMemcpyAsync(pb.d_params, pb.h_params, tpo * sizeof(LevelParams), cudaMemcpyHostToDevice, st));
+      CUDA_OK(c0, cudaMemcpyAsync(pb.d_cta, pb.h_cta, tco * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+      for (auto& t : tl) {
+        Packed pk{pb.d_params + std::get<1>(t), pb.d_cta + std::get<2>(t), (uint32_t)std::get<3>(t)};
+        c0->launches += launch_transpose_packed(std::get<0>(t), pk, std::get<4>(t), st);
+      }
+      CUDA_OK(c0, cudaGetLastError());
+      // the pinned staging is rewritten by the next step only after its uploads: the
+      // copies above are stream-ordered, but the host must not overwrite h_params early
+      CUDA_OK(c0, cudaStreamSynchronize(st));
+    }
+  }
+  // ---- specifications that left the packed loop: solved alone (same code as rei_solve)
+  CUDA_OK(cs[0], cudaStreamSynchronize(st));
+  for (size_t i = 0; i < n; ++i) {
+    if (!sp[i].fallback) continue;
+    Ctx* c = sp[i].c;
+    c->stream = own_streams[i];
+    c->sort_levels = c->mode == DEDUP_BITMAP && getenv("REI_NO_LEVEL_SORT") == nullptr;
+    status[i] = solve_impl(c, max_cost);
+    c->stream = st;
+    done_s[i] = now_s();
+  }
+  for (size_t i = 0; i < n; ++i)  // sort_levels as rei_init set it (the packed steps skip it)
+    sp[i].c->sort_levels = sp[i].c->mode == DEDUP_BITMAP && !sp[i].c->sharded && getenv("REI_NO_LEVEL_SORT") == nullptr;
+  return REI_OK;
+}
+
 }  // namespace
 }  // namespace rei
 
@@ -2153,7 +2526,11 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   for (auto& w : c->N) c->h2d_bytes += w.size() + 4;
   c->d2h_bytes += 64 + 8ull * c->tab.n;  // table summary + IC keys
   c->W32 = next_pow2_words(c->tab.n);
-  c->mode = (c->tab.n <= 32) ? DEDUP_BITMAP : (c->W32 == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
+  // small-cache contexts (many alive at once, f4) keep the 2^|IC|-bit bitmap for
+  // |IC| <= 20 only (<= 128 KB); wider one-word CSs use the two-word 64-bit-key hash set
+  // (the storage width is invisible to results: reading A16)
+  if ((c->flags & REI_FLAG_SMALL_CACHE) && c->W32 == 1 && c->tab.n > 20) c->W32 = 2;
+  c->mode = (c->W32 == 1) ? DEDUP_BITMAP : (c->W32 == 2 ? DEDUP_HASH64 : DEDUP_HASHIDX);
   // wide CSs whose top bits are free keep the whole CS in the slot (one sector per probe,
   // no arena read on a fingerprint match); REI_INDEXED_KEYS=1 keeps fingerprint + index
   if (c->mode == DEDUP_HASHIDX && ((c->W32 == 4 && c->tab.n <= 127) || (c->W32 == 8 && c->tab.n <= 254)) &&
@@ -2208,6 +2585,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   // 2^28 entries); hash modes start at 2^22 entries and grow ahead of each level.
   uint64_t cap0 = 1ull << 22;
   if (c->mode == DEDUP_BITMAP) cap0 = std::min<uint64_t>(1ull << 28, (1ull << c->tab.n) + 64);
+  if (c->flags & REI_FLAG_SMALL_CACHE) cap0 = std::min<uint64_t>(cap0, 1ull << 16);
   // the free-memory query is skipped when the initial cache is < 1/8 of the HBM
   if (c->budget_user || c->sharded || cap0 * bytes_per_entry(c.get()) > device_total_bytes(c->device) / 8)
     cap0 = std::min<uint64_t>(cap0, std::max<uint64_t>(1024, budget_of(c.get()) / bytes_per_entry(c.get())));
@@ -2447,6 +2825,41 @@ rei_status rei_solve_group(void* const* ctxs, int G, uint32_t max_cost, rei_resu
     if (s != REI_OK && s != REI_NOT_FOUND && s != REI_OUT_OF_MEMORY && c->err.empty()) c->err = first_err;
   }
   if (out) *out = g.m[0]->result;
+  return s;
+}
+
+rei_status rei_solve_packed(void* const* ctxs, size_t n, uint32_t max_cost, rei_result* out, rei_status* status,
+                            double* done_seconds) {
+  if (!ctxs || n == 0) return REI_EINVAL;
+  std::vector<Ctx*> cs(n);
+  for (size_t i = 0; i < n; ++i) {
+    cs[i] = static_cast<Ctx*>(ctxs[i]);
+    if (!cs[i] || cs[i]->device != cs[0]->device) return REI_EINVAL;
+  }
+  cudaSetDevice(cs[0]->device);
+  // every context's pending work (rei_init) is done before the shared stream runs
+  for (Ctx* c : cs) cudaStreamSynchronize(c->stream);
+  std::vector<rei_status> st;
+  std::vector<double> done;
+  const auto t0 = std::chrono::steady_clock::now();
+  // every context's work (packed launches, growth, reconstruction) on one stream for
+  // the packed steps; each context's own stream again for a spec solved alone
+  std::vector<cudaStream_t> own(n);
+  for (size_t i = 0; i < n; ++i) { own[i] = cs[i]->stream; cs[i]->stream = cs[0]->stream; }
+  rei_status s = rei::solve_packed(cs, max_cost, st, done, own);
+  for (size_t i = 0; i < n; ++i) cs[i]->stream = own[i];
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  for (size_t i = 0; i < n; ++i) {
+    Ctx* c = cs[i];
+    c->result.seconds = i < done.size() ? done[i] : secs;
+    c->result.regex = c->regex.c_str();
+    uint64_t uniq = 0;
+    for (auto& l : c->stats) uniq += l.unique;
+    c->result.unique = uniq;
+    if (out) out[i] = c->result;
+    if (status) status[i] = i < st.size() ? st[i] : s;
+    if (done_seconds) done_seconds[i] = c->result.seconds;
+  }
   return s;
 }
 

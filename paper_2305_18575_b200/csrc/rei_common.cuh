@@ -107,8 +107,20 @@ struct LevelParams {
                               // level runs) that tentative indexed-hash slots point into
   uint32_t tent;              // kTent in multi-rank levels with the indexed hash set, else 0
   uint32_t pad_t;
+  // packed launches (f4, rei_solve_packed): the per-spec operands of the unary kernel
+  // (? count / arena base, * count / arena base / first slab) and of the transpose
+  // (level count in un_q, arena base in un_bq, first slab in un_slab)
+  uint64_t un_q, un_s, un_bq, un_bs, un_slab;
   uint32_t pos[kMaxW32];
   uint32_t neg[kMaxW32];
+};
+
+// One packed launch serving many specifications: CTA group i =
+// blocks [cta_start[i], cta_start[i+1]) runs specification i with params[i].
+struct Packed {
+  const LevelParams* params;
+  const uint32_t* cta_start;  // [nspec + 1]
+  uint32_t nspec;
 };
 
 #ifdef __CUDACC__

@@ -36,6 +36,17 @@ int launch_union(int W32, const LevelParams& p, cudaStream_t st);
 int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t count, uint32_t* tarena,
                      uint64_t slab_base, cudaStream_t st);
 int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, cudaStream_t st);
+// Packed launches (f4, rei_solve_packed): one grid, CTA group i runs pk.params[i]
+// (W32 in {1, 2} and <= 15 proper splits per word; maxk_class = 1, 3, 7 or 15).
+int packable(int W32, int maxk);
+int maxk_class(int maxk);
+int launch_ctl_reset_packed(const LevelParams* params, uint32_t n, cudaStream_t st);
+int launch_ctl_gather_packed(const LevelParams* params, uint32_t n, LevelCtl* out, cudaStream_t st);
+int launch_concat_packed(int W32, int maxk, bool slice_a, const Packed& pk, uint32_t ctas, size_t max_nblocks,
+                         cudaStream_t st);
+int launch_union_packed(int W32, const Packed& pk, uint32_t ctas, size_t max_nblocks, cudaStream_t st);
+int launch_unary_packed(int W32, int maxk, const Packed& pk, uint32_t ctas, cudaStream_t st);
+int launch_transpose_packed(int W32, const Packed& pk, uint32_t ctas, cudaStream_t st);
 
 // Canonical first-occurrence merge of an all-gathered level list (exchange.cu).
 struct MergeScratch {

@@ -21,6 +21,7 @@ STATUS_NAMES = {0: "found", 1: "invalid", 2: "not_found", 3: "out_of_memory", 4:
 FLAG_COMPLETE_FINAL_LEVEL = 1
 FLAG_NO_ONTHEFLY = 2
 FLAG_SHARDED_CACHE = 4
+FLAG_SMALL_CACHE = 8
 KERNEL_CLASSES = ("precompute", "unary", "concat", "union", "transpose", "other")
 
 
@@ -158,6 +159,9 @@ def load_library():
     lib.rei_solve_batch.restype = c.c_int
     lib.rei_solve_batch.argtypes = [c.POINTER(c.c_void_p), c.c_size_t, c.c_uint32, c.c_int,
                                     c.POINTER(_Result), c.POINTER(c.c_int)]
+    lib.rei_solve_packed.restype = c.c_int
+    lib.rei_solve_packed.argtypes = [c.POINTER(c.c_void_p), c.c_size_t, c.c_uint32, c.POINTER(_Result),
+                                     c.POINTER(c.c_int), c.POINTER(c.c_double)]
     lib.rei_solve_group.restype = c.c_int
     lib.rei_solve_group.argtypes = [c.POINTER(c.c_void_p), c.c_int, c.c_uint32, c.POINTER(_Result)]
     _lib = lib
@@ -219,7 +223,7 @@ class Solver:
                  mem_budget_bytes: int = 0, error: Optional[Tuple[int, int]] = None,
                  complete_final_level: bool = False, world_size: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, max_entries: int = 0, onthefly: bool = True,
-                 sharded_cache: bool = False, allgather=None):
+                 sharded_cache: bool = False, allgather=None, small_cache: bool = False):
         """world_size > 1 (one process per rank, rei_solve collective): the level
         exchange runs over NCCL with `nccl_id` (rank 0's nccl_unique_id()), or, with
         `allgather` and no nccl_id, through that host all-gather (bytes -> list of
@@ -255,7 +259,8 @@ class Solver:
         else:
             opts.err_num, opts.err_den = 0, 1
         opts.flags = (FLAG_COMPLETE_FINAL_LEVEL if complete_final_level else 0) | \
-            (0 if onthefly else FLAG_NO_ONTHEFLY) | (FLAG_SHARDED_CACHE if sharded_cache else 0)
+            (0 if onthefly else FLAG_NO_ONTHEFLY) | (FLAG_SHARDED_CACHE if sharded_cache else 0) | \
+            (FLAG_SMALL_CACHE if small_cache else 0)
         opts.max_entries = int(max_entries)
         opts.world_size, opts.rank = int(world_size), int(rank)
         costs_c = _Costs(*[int(c) for c in costs])
@@ -510,6 +515,29 @@ def solve_batch(solvers: Sequence["Solver"], max_cost: int = 500, threads: int =
                           r.last_complete_cost, r.candidates, r.cand_complete, r.unique, r.seconds,
                           r.n_ic, r.cs_words, s.level_stats()))
     return out
+
+
+def solve_packed(solvers: Sequence["Solver"], max_cost: int = 500) -> Tuple[List[Result], List[float]]:
+    """Packed launches over many small specifications on one device (f4, include/rei.h
+    rei_solve_packed): results, and each spec's host seconds from the call to its result."""
+    lib = load_library()
+    n = len(solvers)
+    arr = (ctypes.c_void_p * max(1, n))(*[s._h.value for s in solvers])
+    res = (_Result * max(1, n))()
+    sts = (ctypes.c_int * max(1, n))()
+    done = (ctypes.c_double * max(1, n))()
+    st = lib.rei_solve_packed(arr, n, int(max_cost), res, sts, done)
+    if st != REI_OK:
+        raise ReiError(st, solvers[0]._err() if solvers else "")
+    out = []
+    for i, s in enumerate(solvers):
+        r, sti = res[i], sts[i]
+        if sti not in (REI_OK, REI_NOT_FOUND, REI_OUT_OF_MEMORY):
+            raise ReiError(sti, s._err())
+        out.append(Result(STATUS_NAMES[sti], (r.regex or b"").decode("latin-1"), r.cost,
+                          r.last_complete_cost, r.candidates, r.cand_complete, r.unique, r.seconds,
+                          r.n_ic, r.cs_words, s.level_stats()))
+    return out, [done[i] for i in range(n)]
 
 
 def solve(spec, max_cost: int = 500, **kw) -> Result:

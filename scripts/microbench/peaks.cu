@@ -88,7 +88,9 @@ __global__ void k_gather(const unsigned long long* __restrict__ tab, unsigned lo
     for (int k = 0; k < K; ++k) {
       st = mix(st + k + 1);
       const unsigned long long* p = tab + (st & (nsect - 1)) * 4;
-      if (BYTES == 8) {
+      if (BYTES == 4) {  // (label 4 = a plain 8-byte load, L1-allocating, like the hash probes)
+        v[k] = *p;
+      } else if (BYTES == 8) {
         v[k] = *(const volatile unsigned long long*)p;
       } else if (BYTES == 16) {
         const ulonglong2 q = *reinterpret_cast<const ulonglong2*>(p);
@@ -268,9 +270,32 @@ int main3() {
   return 0;
 }
 
+// The random-read kernel variants once each, for an ncu capture of DRAM bytes per read:
+// volatile 8-byte, plain 8-byte, 16-byte and 32-byte reads from a 16 GiB table.
+int main4() {
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, 0));
+  g_sms = prop.multiProcessorCount;
+  size_t freeb, totalb;
+  CK(cudaMemGetInfo(&freeb, &totalb));
+  size_t maxb = 16ull << 30;
+  while (maxb > freeb * 8 / 10) maxb >>= 1;
+  unsigned long long* tab;
+  CK(cudaMalloc(&tab, maxb));
+  k_fill<<<g_sms * 8, 256>>>(tab, maxb / 8);
+  CK(cudaDeviceSynchronize());
+  run_gather<8, 8>(tab, maxb, 8, true);
+  run_gather<8, 4>(tab, maxb, 8, true);
+  run_gather<8, 16>(tab, maxb, 8, true);
+  run_gather<8, 32>(tab, maxb, 8, true);
+  CK(cudaFree(tab));
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && argv[1][0] == '2') return main2();
   if (argc > 1 && argv[1][0] == '3') return main3();
+  if (argc > 1 && argv[1][0] == '4') return main4();
   cudaDeviceProp prop;
   CK(cudaGetDeviceProperties(&prop, 0));
   g_sms = prop.multiProcessorCount;

@@ -304,6 +304,37 @@ def c2_instances(count: int = 8, seed0: int = 0, le: int = 6, p: int = 10, n: in
     return out
 
 
+# The many-small-specifications suite, after the paper's benchmark
+# suites (Type 1 with p, n in 8..12; Type 2 with p, n in 7..14; binary;
+# 12 cost functions).  Lengths are capped (le = 4, |IC| <= 31) so that
+# every spec is a small, latency-bound search; the cost functions rotate through the
+# paper's single-expensive-constructor family.
+SUITE_COSTS = [(1, 1, 1, 1, 1), (1, 1, 10, 1, 1), (1, 10, 1, 1, 1), (1, 1, 1, 10, 1),
+               (10, 1, 1, 1, 1), (1, 1, 1, 1, 10)]
+
+
+def suite_f4(count: int = 1024, seed0: int = 0) -> List[Spec]:
+    """`count` seeded specs: alternately Type 1 (le 4, p, n in 8..12) and Type 2
+    (le 4, p, n in 7..14), cost functions from SUITE_COSTS.  Infeasible draws are
+    skipped."""
+    rng = SplitMix64(seed0 ^ 0x5EED5)
+    out: List[Spec] = []
+    i = 0
+    while len(out) < count:
+        costs = SUITE_COSTS[i % len(SUITE_COSTS)]
+        le = 4
+        try:
+            if i % 2 == 0:
+                sp = gen_type1("01", le, 8 + rng.below(5), 8 + rng.below(5), seed0 + i, costs=costs)
+            else:
+                sp = gen_type2("01", le, 7 + rng.below(8), 7 + rng.below(8), seed0 + i, costs=costs)
+            out.append(sp)
+        except InfeasibleParams:
+            pass
+        i += 1
+    return out
+
+
 # Planted wide-IC instances (BASELINE configs[2], configs[3]); parameters fixed
 # here so every side regenerates byte-identical specs.
 C3_PLANTED = [

@@ -189,6 +189,20 @@ def test_ic_over_512_is_einval_and_device_stays_usable():
     assert (rg.status, rg.cost) == (ro.status, ro.cost)
 
 
+@pytest.mark.parametrize("sp,K", RANDOM_W1[:4] + RANDOM_W1[12:14] + W2[:1], ids=ids(RANDOM_W1[:4] + RANDOM_W1[12:14] + W2[:1]))
+def test_small_cache_parity(sp, K):
+    # REI_FLAG_SMALL_CACHE: the cache starts at 2^16 entries and grows; |IC| in 21..32
+    # runs on the two-word 64-bit-key hash set instead of the 2^|IC|-bit bitmap
+    o = oracle.Oracle.from_spec(sp)
+    ro = o.solve(K, complete_final_level=True)
+    g = gpu_solver(sp, complete_final_level=True, small_cache=True)
+    rg = g.solve(K)
+    assert (rg.status, rg.cost) == (ro.status, ro.cost)
+    last = ro.cost if ro.status == "found" else K
+    for c in range(1, last + 1):
+        assert sorted(g.level_cs(c)) == sorted(o.level_cs(c)), c
+
+
 @pytest.mark.parametrize("var", ["REI_GENERIC_CONCAT", "REI_GENERIC_UNARY"])
 @pytest.mark.parametrize("sp,K", RANDOM_W1[:3] + W2[:2] + W4[:1] + W8[:1],
                          ids=ids(RANDOM_W1[:3] + W2[:2] + W4[:1] + W8[:1]))
