@@ -43,15 +43,34 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def _build_locked(verbose: bool) -> str:
-    cmd = [NVCC, *ARCH, *FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, f) for f in SOURCES]]
+    # one nvcc per translation unit, in parallel, then one link
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(PKG, "build")
+    os.makedirs(objdir, exist_ok=True)
+    comp = [f for f in FLAGS if f not in ("--shared", "-ldl")]
+
+    def compile_one(f):
+        obj = os.path.join(objdir, f.replace(".cu", ".o"))
+        cmd = [NVCC, *ARCH, *comp, "-c", "-o", obj, os.path.join(CSRC, f)]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        outs = list(ex.map(compile_one, SOURCES))
+    report = ""
+    for obj, r in outs:
+        report += r.stderr
+        if r.returncode != 0:
+            sys.stderr.write(r.stdout + r.stderr)
+            raise RuntimeError("nvcc failed building librei_b200.so")
+    cmd = [NVCC, *ARCH, "--shared", "-Xcompiler", "-fPIC", "-o", LIB + ".tmp", *[o for o, _ in outs], "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building librei_b200.so")
+        raise RuntimeError("nvcc failed linking librei_b200.so")
     with open(os.path.join(PKG, "ptxas_report.txt"), "w") as f:
-        f.write(r.stderr)
+        f.write(report)
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write(report)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

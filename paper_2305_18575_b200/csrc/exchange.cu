@@ -261,14 +261,21 @@ bool merge_level(int W32, const uint32_t* g_cs, const unsigned long long* g_bp, 
 // level is free: it is fixed before the level is used as an operand, back-pointers
 // refer to operand indices in that order, and every rank sorts identically.
 bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, MergeScratch& s, cudaStream_t st,
-                std::string& err, uint64_t* launches) {
+                std::string& err, uint64_t* launches, bool may_skip) {
   if (m < 2) return true;
   if (m >= 0xffffffffull) { err = "level too large to sort"; return false; }
   const int grid = (int)std::min<uint64_t>((m + 255) / 256, 148 * 8);
   bool ok = ensure<unsigned long long>(&s.keys, &s.keys_cap, m * 8, st) &&
             ensure<unsigned long long>(&s.keys2, &s.keys2_cap, m * 8, st) &&
             ensure<uint32_t>(&s.pos, &s.pos_cap, m * 4, st) && ensure<uint32_t>(&s.pos2, &s.pos2_cap, m * 4, st);
-  if (!ok) { err = "level sort scratch allocation failed"; return false; }
+  if (!ok) {
+    // the order is only a locality optimisation: a single rank short of memory keeps
+    // the level as appended (ranks of one search must all sort, so they fail instead)
+    cudaGetLastError();
+    if (may_skip) return true;
+    err = "level sort scratch allocation failed";
+    return false;
+  }
   auto* keys = static_cast<uint32_t*>(s.keys);
   auto* keys2 = static_cast<uint32_t*>(s.keys2);
   auto* pos = static_cast<uint32_t*>(s.pos);
@@ -281,7 +288,12 @@ bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, Me
   const char* sb = getenv("REI_LEVEL_SORT_BITS");
   const int begin_bit = std::max(0, end_bit - (sb ? atoi(sb) : 12));
   cub::DeviceRadixSort::SortPairs(nullptr, t1, keys, keys2, pos, pos2, (int)m, begin_bit, end_bit, st);
-  if (!ensure<uint8_t>(&s.temp, &s.temp_cap, t1, st)) { err = "cub temp"; return false; }
+  if (!ensure<uint8_t>(&s.temp, &s.temp_cap, t1, st)) {
+    cudaGetLastError();
+    if (may_skip) return true;
+    err = "cub temp";
+    return false;
+  }
   if (cub::DeviceRadixSort::SortPairs(s.temp, t1, keys, keys2, pos, pos2, (int)m, begin_bit, end_bit, st) !=
       cudaSuccess) {
     err = "level sort failed";

@@ -1774,6 +1774,277 @@ __global__ void k_rehash(LevelParams p, unsigned long long base, unsigned long l
   }
 }
 
+// ============================================================================
+// Device-resident level loop (DevLoop, rei_common.cuh): the small, launch-bound levels
+// of a search in ONE persistent cooperative grid.  Per level: thread (0, 0) finishes
+// the previous level (its size from the control line) and plans the next one exactly
+// like the host's plan_level (Q | S | C by L ascending | U by L ascending, ranks
+// row-major, U with L = R triangular); after a grid barrier every thread takes
+// candidates by rank (one per thread: the operands, the CS operation -- `?` sets the
+// epsilon bit, `*` the shortlex fixpoint pass, concatenation the guide-table fold
+// (Alg. 2), union the OR -- then the same dedup / precision / append tail
+// as the level kernels).  The previous level is transposed into slabs meanwhile.
+// The loop hands the search back to the host before a level with more than
+// cand_limit candidates, one that could overflow the cache, one whose plan has too
+// many blocks, after a level the host must sort (bitmap mode, >= sort_min entries),
+// at the first precise candidate, or past max_cost.
+
+// arrive-and-wait over the whole (co-resident, cooperative) grid
+__device__ __forceinline__ void grid_sync(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// concatenation A.B of two CSs, one thread: bit w = A[eps] B[w] | A[w] B[eps] |
+// OR over the proper splits (u, v) of w of A[u] B[v] (Alg. 2 / P:637)
+template <int W>
+__device__ void concat_cs(const uint32_t (&a)[W], const uint32_t (&b)[W], uint32_t (&r)[W], uint32_t n,
+                          const uint32_t* s_split, const uint32_t* s_nsplit, int NW) {
+  const bool ae = a[0] & 1u, be = b[0] & 1u;
+#pragma unroll
+  for (int q = 0; q < W; ++q) r[q] = (ae ? b[q] : 0u) | (be ? a[q] : 0u);
+  for (uint32_t w = 1; w < n; ++w) {
+    if (get_bit<W>(r, w)) continue;
+    const uint32_t m = s_nsplit[w];
+    for (uint32_t k = 0; k < m; ++k) {
+      const uint32_t sp = s_split[k * NW + w];
+      if (get_bit<W>(a, sp >> 16) & get_bit<W>(b, sp & 0xffffu)) {
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+          if ((w >> 5) == (uint32_t)q) r[q] |= 1u << (w & 31);
+        break;
+      }
+    }
+  }
+}
+
+// thread (0, 0): finish level st.cost, plan the next non-empty level
+__device__ void loop_plan(const DevLoop& d, LevelCtl* ctl) {
+  LoopState& st = *d.st;
+  const uint32_t c_done = st.cost;
+  bool transpose_done = false;
+  st.tr_count = 0;
+  if (c_done) {
+    const unsigned long long size = *(volatile unsigned long long*)&ctl->count;
+    const bool overflow = *(volatile unsigned int*)&ctl->overflow != 0;
+    const unsigned long long found = *(volatile unsigned long long*)&ctl->found_rank;
+    d.lvl_eval[c_done] = *(volatile unsigned long long*)&ctl->evaluated;
+    d.lvl_ns[c_done] = global_ns() - st.t_level;
+    if (overflow) {  // partial level: the host clears it and redoes it
+      st.stop = LOOP_OVERFLOW;
+      st.next_cost = c_done;
+      return;
+    }
+    d.lvl_size[c_done] = size;
+    d.lvl_begin[c_done] = st.arena_used;
+    d.lvl_slab[c_done] = st.slabs_used;
+    st.last_cost = c_done;
+    if (found != ~0ull) {
+      st.found_rank = found;
+      st.arena_used += size;
+      st.stop = LOOP_FOUND;
+      st.next_cost = c_done;
+      return;
+    }
+    const bool sort = d.sort_min && size >= d.sort_min;
+    if (!sort) {  // transposed this round by every CTA
+      st.tr_base = st.arena_used;
+      st.tr_count = size;
+      st.tr_slab = st.slabs_used;
+      st.slabs_used += (size + 31) / 32;
+    }
+    st.arena_used += size;
+    if (sort) {  // the host sorts it (its order must be fixed before it is an operand)
+      st.stop = LOOP_SORT;
+      st.next_cost = c_done + 1;
+      return;
+    }
+    transpose_done = true;
+  }
+  (void)transpose_done;
+  // the next level with a non-empty plan
+  const int c1 = (int)d.c1;
+  auto size_of = [&](int L) -> unsigned long long { return L >= c1 ? d.lvl_size[L] : 0ull; };
+  for (uint32_t c = c_done ? c_done + 1 : d.first_cost; c <= d.max_cost; ++c) {
+    d.lvl_size[c] = 0;
+    const int cost = (int)c;
+    unsigned long long off = 0, items = 0;
+    uint32_t nb = 0;
+    bool too_many = false;
+    auto add = [&](uint32_t kind, unsigned long long a_base, unsigned long long b_base, unsigned long long na,
+                   unsigned long long nbb, unsigned long long cnt, bool tri) {
+      if (nb == kLoopMaxBlocks) { too_many = true; return; }
+      Block b{};
+      b.kind = kind;
+      b.tri = tri ? 1u : 0u;
+      b.a_base = a_base;
+      b.b_base = b_base;
+      b.na = na;
+      b.nb = nbb;
+      b.cand_off = off;
+      b.cand_count = cnt;
+      b.item_off = items;
+      d.blocks[nb++] = b;
+      off += cnt;
+      items += (kind == BK_Q || kind == BK_S) ? na : (tri ? na * na : na * nbb);
+    };
+    const int lq = cost - (int)d.k_opt, ls = cost - (int)d.k_star;
+    const unsigned long long nq = size_of(lq), ns = size_of(ls);
+    if (nq) add(BK_Q, d.lvl_begin[lq], 0, nq, 0, nq, false);
+    if (ns) add(BK_S, d.lvl_begin[ls], 0, ns, 0, ns, false);
+    for (int L = c1; L <= cost - (int)d.k_cat - c1; ++L) {
+      const int R = cost - (int)d.k_cat - L;
+      const unsigned long long na = size_of(L), nbb = size_of(R);
+      if (na && nbb) add(BK_C, d.lvl_begin[L], d.lvl_begin[R], na, nbb, na * nbb, false);
+    }
+    for (int L = c1; L <= cost - (int)d.k_alt - L; ++L) {
+      const int R = cost - (int)d.k_alt - L;
+      const unsigned long long na = size_of(L), nbb = size_of(R);
+      if (!na || !nbb) continue;
+      const bool tri = L == R;
+      const unsigned long long cnt = tri ? na * (na - 1) / 2 : na * nbb;
+      if (cnt) add(BK_U, d.lvl_begin[L], d.lvl_begin[R], na, nbb, cnt, tri);
+    }
+    if (!nb && !too_many) continue;  // no level at this cost
+    st.next_cost = c;
+    if (too_many) { st.stop = LOOP_BLOCKS; return; }
+    if (off > d.cand_limit) { st.stop = LOOP_BIG; return; }
+    if (st.arena_used + off > d.entry_limit || st.slabs_used + (off + 31) / 32 + 1 > d.slab_limit) {
+      st.stop = LOOP_CAPACITY;
+      return;
+    }
+    st.cost = c;
+    st.nblocks = nb;
+    st.items = items;
+    st.out_base = st.arena_used;
+    ctl->count = 0;
+    ctl->evaluated = 0;
+    ctl->eval_c = 0;
+    ctl->eval_u = 0;
+    st.t_level = global_ns();
+    return;
+  }
+  st.stop = LOOP_MAXCOST;
+  st.next_cost = d.max_cost + 1;
+}
+
+template <int W>
+__global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
+  constexpr int NW = 32 * W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint32_t* s_split = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* s_nsplit = s_split + p0.maxk * NW;
+  __shared__ LevelParams sp;
+  __shared__ Block s_blocks[kLoopMaxBlocks];
+  __shared__ unsigned long long s_items, s_tr_base, s_tr_count, s_tr_slab;
+  __shared__ uint32_t s_nblocks, s_stop;
+  for (int i = threadIdx.x; i < (int)(p0.maxk * NW); i += blockDim.x)
+    s_split[i] = p0.split[(i / NW) * kMaxNW + (i % NW)];
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p0.nsplit[i];
+  if (threadIdx.x == 0) sp = p0;
+  const uint32_t lane = lane_id();
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long nthreads = (unsigned long long)gridDim.x * blockDim.x;
+  for (;;) {
+    grid_sync(d.bar);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      loop_plan(d, p0.ctl);
+      __threadfence();
+    }
+    grid_sync(d.bar);
+    if (threadIdx.x == 0) {
+      const volatile LoopState* vs = d.st;
+      s_stop = vs->stop;
+      s_nblocks = vs->nblocks;
+      s_items = vs->items;
+      s_tr_base = vs->tr_base;
+      s_tr_count = vs->tr_count;
+      s_tr_slab = vs->tr_slab;
+      sp.out_base = vs->out_base;
+    }
+    __syncthreads();
+    if (s_tr_count)
+      transpose_body<W>(p0.arena, s_tr_base, s_tr_count, const_cast<uint32_t*>(p0.tarena), s_tr_slab, blockIdx.x,
+                        gridDim.x);
+    if (s_stop != LOOP_RUN) break;
+    for (int i = threadIdx.x; i < (int)(s_nblocks * sizeof(Block) / 4); i += blockDim.x)
+      reinterpret_cast<uint32_t*>(s_blocks)[i] = __ldcg(reinterpret_cast<const uint32_t*>(d.blocks) + i);
+    __syncthreads();
+    const unsigned long long items = s_items;
+    const int nb = (int)s_nblocks;
+    uint32_t evaluated = 0;
+    for (unsigned long long base = tid - lane; base < items; base += nthreads) {
+      if (found_and_stop(sp)) break;
+      const unsigned long long item = base + lane;
+      bool valid = item < items;
+      uint32_t cs[1][W];
+      bool skip = false;
+      unsigned long long rank = 0;
+      if (valid) {
+        const Block& b = s_blocks[find_block(s_blocks, nb, item)];
+        const unsigned long long local = item - b.item_off;
+        uint32_t x[W], y[W];
+        if (b.kind == BK_Q || b.kind == BK_S) {
+          load_cs<W>(p0.arena, b.a_base + local, x);
+          if (b.kind == BK_Q) {
+#pragma unroll
+            for (int q = 0; q < W; ++q) cs[0][q] = x[q] | (q == 0 ? 1u : 0u);
+          } else {
+            star_cs<W>(x, cs[0], p0.n, s_split, s_nsplit, NW);
+          }
+          rank = b.cand_off + local;
+          skip = cs_equal<W>(cs[0], x);
+        } else {
+          const unsigned long long ncol = b.tri ? b.na : b.nb;
+          const unsigned long long i = local / ncol, j = local % ncol;
+          if (b.tri && i >= j) {
+            valid = false;
+          } else {
+            load_cs<W>(p0.arena, b.a_base + i, x);
+            load_cs<W>(p0.arena, b.b_base + j, y);
+            if (b.kind == BK_C) {
+              concat_cs<W>(x, y, cs[0], p0.n, s_split, s_nsplit, NW);
+            } else {
+#pragma unroll
+              for (int q = 0; q < W; ++q) cs[0][q] = x[q] | y[q];
+            }
+            rank = b.cand_off + (b.tri ? i * b.na - i * (i + 1) / 2 + (j - i - 1) : i * b.nb + j);
+            skip = cs_equal<W>(cs[0], x) || cs_equal<W>(cs[0], y);
+          }
+        }
+      }
+      if (!valid) {
+#pragma unroll
+        for (int q = 0; q < W; ++q) cs[0][q] = 0;
+      }
+      evaluated += valid ? 1u : 0u;
+      const bool v1[1] = {valid}, k1[1] = {skip};
+      process_batch<W, 1>(sp, cs, v1, k1, [&](int) { return rank; });
+    }
+    const uint32_t tot = __reduce_add_sync(__activemask(), evaluated);
+    if (lane == (uint32_t)(__ffs(__activemask()) - 1) && tot) atomicAdd(&p0.ctl->evaluated, (unsigned long long)tot);
+  }
+}
+
 // Device CS operations on explicit operand pairs (tests): thread per pair, direct
 // fold over the full guide table (epsilon splits + proper splits).
 template <int W>
@@ -2133,6 +2404,31 @@ int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, 
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                uint64_t count, cudaStream_t st) {
   REI_DISPATCH_W(W32, return launch_ops_t<W>(p, op, a, b, out, count, st));
+}
+
+// One cooperative launch of the device level loop; returns 1 (launched) or 0 (not
+// eligible: width, or the grid cannot be co-resident).
+int launch_level_loop(int W32, const LevelParams& p, const DevLoop& d, cudaStream_t st) {
+  auto go = [&](auto w) -> int {
+    constexpr int W = decltype(w)::value;
+    const size_t smem = (size_t)p.maxk * 32 * W * 4 + 32 * W * 4;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_level_loop<W>, 256, smem) != cudaSuccess || occ < 1)
+      return 0;
+    int grid = sm_count() * std::min(occ, 2);
+    LevelParams pp = p;
+    DevLoop dd = d;
+    void* args[] = {&pp, &dd};
+    if (cudaLaunchCooperativeKernel((const void*)k_level_loop<W>, dim3(grid), dim3(256), args, smem, st) !=
+        cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    return 1;
+  };
+  if (W32 == 1) return go(std::integral_constant<int, 1>{});
+  if (W32 == 2) return go(std::integral_constant<int, 2>{});
+  return 0;
 }
 
 }  // namespace rei

@@ -201,6 +201,11 @@ struct Ctx {
   XScratch xs;
   MergeScratch merge;
 
+  // device level loop (DevLoop): device arrays + pinned mirror, same layout
+  void* d_loop = nullptr;
+  void* h_loop = nullptr;
+  size_t loop_bytes = 0;
+
   // profiling
   uint64_t h2d_bytes = 0, d2h_bytes = 0;
   uint64_t launches = 0;
@@ -229,8 +234,9 @@ struct Ctx {
     for (void* q : {(void*)arena, (void*)bp, (void*)tarena, (void*)bitmap, (void*)table, (void*)special,
                     (void*)ctl_base, (void*)d_blocks, (void*)d_peers, (void*)tab.split, (void*)tab.nsplit,
                     (void*)tab.word_len, (void*)tab.seeds, (void*)d_ctl_all, (void*)st_cs, (void*)st_bp,
-                    (void*)d_small, (void*)d_small_all})
+                    (void*)d_small, (void*)d_small_all, d_loop})
       dfree(q);
+    host_free(h_loop);
     host_free(h_peers);
     host_free(h_ctl);
     host_free(h_blocks);
@@ -751,6 +757,164 @@ rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
   }
   c->regex = rx;
   c->result.cost = (uint32_t)cost;
+  return REI_OK;
+}
+
+// Device level loop (k_level_loop): levels c1 + 1 .. while they are
+// small run inside one cooperative kernel with no host round trip per level.  On
+// return the finished levels are in c->levels / c->stats exactly as the host loop
+// would have left them (plans recomputed by plan_level from the level sizes, so
+// back-pointer ranks decode identically); *next = the level the host loop continues
+// with; *done = the search ended (a precise candidate).
+bool device_loop_ok(const Ctx* c, uint32_t max_cost) {
+  return !c->sharded && !c->otf_level && c->world == 1 && (c->mode == DEDUP_BITMAP || c->mode == DEDUP_HASH64) &&
+         c->W32 <= 2 && max_cost <= 65535 && getenv("REI_NO_DEVICE_LOOP") == nullptr;
+}
+
+rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, bool* done) {
+  *done = false;
+  const rei_costs& k = c->costs;
+  const int c1 = (int)k.sym;
+  *next = c1 + 1;
+  if ((int)max_cost <= c1) return REI_OK;
+  const size_t L = (size_t)max_cost + 1;
+  const size_t arr = L * 8;
+  const size_t off_blocks = 5 * arr;
+  const size_t off_state = off_blocks + sizeof(Block) * kLoopMaxBlocks;
+  const size_t off_bar = off_state + sizeof(LoopState);
+  const size_t bytes = off_bar + 64;
+  if (c->loop_bytes < bytes) {
+    c->dfree(c->d_loop);
+    host_free(c->h_loop);
+    c->d_loop = nullptr;
+    c->h_loop = nullptr;
+    c->loop_bytes = 0;
+    if (c->dmalloc(&c->d_loop, bytes) != cudaSuccess || host_alloc(&c->h_loop, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return REI_OK;  // the host loop runs every level instead
+    }
+    c->loop_bytes = bytes;
+  }
+  auto* h = static_cast<uint8_t*>(c->h_loop);
+  auto* dv = static_cast<uint8_t*>(c->d_loop);
+  auto* h_size = reinterpret_cast<unsigned long long*>(h);
+  auto* h_begin = h_size + L;
+  auto* h_slab = h_begin + L;
+  auto* h_eval = h_slab + L;
+  auto* h_ns = reinterpret_cast<long long*>(h_eval + L);
+  auto* h_st = reinterpret_cast<LoopState*>(h + off_state);
+  memset(h, 0, bytes);
+  const LevelInfo& l1 = c->levels.at(c1);
+  h_size[c1] = l1.size;
+  h_begin[c1] = l1.begin;
+  h_slab[c1] = l1.slab;
+  h_st->arena_used = c->arena_used;
+  h_st->slabs_used = c->slabs_used;
+  h_st->found_rank = ~0ull;
+  CUDA_OK(c, cudaMemcpyAsync(dv, h, bytes, cudaMemcpyHostToDevice, c->stream));
+  c->h2d_bytes += bytes;
+  rei_status s;
+  if ((s = reset_ctl(c)) != REI_OK) return s;
+  LevelParams p;
+  fill_params(c, p);
+  DevLoop d{};
+  d.lvl_size = reinterpret_cast<unsigned long long*>(dv);
+  d.lvl_begin = d.lvl_size + L;
+  d.lvl_slab = d.lvl_begin + L;
+  d.lvl_eval = d.lvl_slab + L;
+  d.lvl_ns = reinterpret_cast<long long*>(d.lvl_eval + L);
+  d.blocks = reinterpret_cast<Block*>(dv + off_blocks);
+  d.st = reinterpret_cast<LoopState*>(dv + off_state);
+  d.bar = reinterpret_cast<unsigned int*>(dv + off_bar);
+  const char* ev = getenv("REI_DEVICE_LOOP_CAND");
+  d.cand_limit = ev ? strtoull(ev, nullptr, 10) : (1ull << 20);
+  d.entry_limit = p.cap;
+  d.slab_limit = c->slab_cap;
+  d.sort_min = c->sort_levels ? (1ull << 14) : 0;
+  d.c1 = (uint32_t)c1;
+  d.first_cost = (uint32_t)c1 + 1;
+  d.max_cost = max_cost;
+  d.k_opt = k.opt;
+  d.k_star = k.star;
+  d.k_cat = k.cat;
+  d.k_alt = k.alt;
+  EventPair ep;
+  c->begin_kernel(REI_K_OTHER, ep);
+  const int n = launch_level_loop(c->W32, p, d, c->stream);
+  c->end_kernel(ep, n);
+  if (!n) {  // not co-resident / not supported: the host loop runs every level
+    double ms;
+    CUDA_OK(c, cudaStreamSynchronize(c->stream));
+    c->collect_events(&ms);
+    return REI_OK;
+  }
+  CUDA_OK(c, cudaMemcpyAsync(h, dv, off_state + sizeof(LoopState), cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OK(c, cudaStreamSynchronize(c->stream));
+  c->d2h_bytes += off_state + sizeof(LoopState);
+  double loop_ms = 0;
+  c->collect_events(&loop_ms);
+  const LoopState S = *h_st;
+  if (getenv("REI_TRACE"))
+    fprintf(stderr, "[rei_solve] device loop levels %d..%u stop %u next %u: %.3f ms\n", c1 + 1, S.last_cost, S.stop,
+            S.next_cost, loop_ms);
+  std::vector<Block> cat, uni;
+  for (int cost = c1 + 1; cost <= (int)S.last_cost; ++cost) {
+    LevelInfo lv;
+    lv.cost = cost;
+    uint64_t nq, ns, ncat, nuni;
+    plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);
+    if (lv.plan.empty()) continue;
+    lv.begin = h_begin[cost];
+    lv.size = h_size[cost];
+    lv.slab = h_slab[cost];
+    const bool found_here = S.stop == LOOP_FOUND && cost == (int)S.last_cost;
+    const uint64_t total = nq + ns + ncat + nuni;
+    rei_level_stat st{};
+    st.cost = (uint32_t)cost;
+    st.cand_q = nq; st.cand_s = ns; st.cand_c = ncat; st.cand_u = nuni;
+    st.unique = lv.size;
+    st.ms = h_ns[cost] * 1e-6;
+    const bool complete = !found_here || (c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL);
+    st.complete = complete ? 1 : 0;
+    st.evaluated = complete ? total : h_eval[cost];
+    st.eval_c = complete ? ncat : 0;
+    st.eval_u = complete ? nuni : 0;
+    c->levels[cost] = lv;
+    c->stats.push_back(st);
+    if (found_here) {
+      c->arena_used = lv.begin + lv.size;
+      c->result.candidates = *cand + st.evaluated;
+      if (complete) {
+        c->result.last_complete_cost = (uint32_t)cost;
+        c->result.cand_complete = *cand + st.evaluated;
+      }
+      *done = true;
+      return finish_found(c, cost, S.found_rank);
+    }
+    *cand += total;
+    c->result.cand_complete = *cand;
+    c->result.candidates = *cand;
+    c->result.last_complete_cost = (uint32_t)cost;
+  }
+  c->arena_used = S.arena_used;
+  c->slabs_used = S.slabs_used;
+  *next = (int)S.next_cost;
+  if (S.stop == LOOP_OVERFLOW) return rebuild_dedup(c, c->arena_used);  // drop the partial level
+  if (S.stop == LOOP_SORT) {  // the host orders the last level, then transposes it
+    LevelInfo& lv = c->levels.at((int)S.last_cost);
+    std::string err;
+    if (!sort_level((uint32_t)c->tab.n, c->arena + lv.begin, c->bp + lv.begin, lv.size, c->merge, c->stream, err,
+                    &c->launches, true)) {
+      c->err = err;
+      return REI_ECUDA;
+    }
+    lv.slab = c->slabs_used;
+    EventPair et;
+    c->begin_kernel(REI_K_TRANSPOSE, et);
+    const int nt = launch_transpose(c->W32, c->arena, lv.begin, lv.size, c->tarena, lv.slab, c->stream);
+    c->end_kernel(et, nt);
+    c->slabs_used += (lv.size + 31) / 32;
+  }
   return REI_OK;
 }
 
@@ -1277,11 +1441,18 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     c->result.cand_complete = cand;
   }
 
+  int first_cost = c1 + 1;
+  if (!multi && g.m.size() == 1 && device_loop_ok(c0, max_cost)) {
+    bool done = false;
+    if ((s = device_levels(c0, max_cost, &first_cost, &cand, &done)) != REI_OK) return s;
+    if (done) return REI_OK;
+  }
+
   std::vector<Block> cat, uni;
   std::vector<LevelCtl> all;
   const bool trace = getenv("REI_TRACE") != nullptr;
   auto t_level = std::chrono::steady_clock::now();
-  for (int cost = c1 + 1; cost <= (int)max_cost; ++cost) {
+  for (int cost = first_cost; cost <= (int)max_cost; ++cost) {
     if (c0->otf_level && needs_uncached(c0, cost)) {
       // OnTheFly mode needs a level it did not cache: stop
       for (Ctx* c : g.m) c->result.candidates = c->result.cand_complete;
@@ -1445,7 +1616,7 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
       if (c->sort_levels && lv.size >= (1u << 14) && !redundant) {  // bitmap mode: order by bitmap position
         std::string err;
         if (!sort_level((uint32_t)c->tab.n, c->arena + lv.begin, c->bp + lv.begin, lv.size, c->merge, c->stream,
-                        err, &c->launches)) {
+                        err, &c->launches, g.world == 1)) {
           c->err = err;
           return REI_ECUDA;
         }
@@ -2561,6 +2732,9 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     // less when concat has priority).
     const char* ev = getenv("REI_CONCURRENT");
     c->concurrency = ev ? std::max(0, std::min(6, atoi(ev))) : (c->mode == DEDUP_BITMAP ? 2 : 3);
+    // small-cache contexts (f4: hundreds alive at once, small levels) run one stream:
+    // ~1000 priority streams in one process made stream creation fail on B200
+    if ((c->flags & REI_FLAG_SMALL_CACHE) && !ev) c->concurrency = 0;
     const int nstreams = std::min(3, c->concurrency);
     if (nstreams >= 1) {
       int prio_lo = 0, prio_hi = 0;

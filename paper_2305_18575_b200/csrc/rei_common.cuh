@@ -115,6 +115,49 @@ struct LevelParams {
   uint32_t neg[kMaxW32];
 };
 
+// Device-resident level loop (k_level_loop): the launch-bound small levels of a search
+// run inside ONE persistent kernel -- plan (Alg. 1 lines 5-8), candidates, dedup,
+// precision, append, transpose -- with grid barriers between levels instead of a host
+// round trip per level.  Thread (0, 0) plans every level exactly as the host's
+// plan_level flattens it (Q | S | C by L | U by L), so back-pointer ranks decode the
+// same way.  State shared by the CTAs lives in `LoopState` (device memory).
+struct LoopState {
+  unsigned long long arena_used, slabs_used;  // cache fill (entries, slabs)
+  unsigned long long out_base;                // arena index of the level being built
+  unsigned long long items;                   // work items of that level
+  unsigned long long tr_base, tr_count, tr_slab;  // level to transpose this round (count 0 = none)
+  unsigned long long found_rank;              // copy of the level's ctl found_rank at stop
+  long long t_level;                          // %globaltimer at the level's start
+  uint32_t cost;                              // level being built (0 = none yet)
+  uint32_t next_cost;                         // where the host continues
+  uint32_t stop;                              // LoopStop
+  uint32_t nblocks;
+  uint32_t last_cost;                         // last level finished (complete or found)
+  uint32_t pad;
+};
+enum LoopStop : uint32_t {
+  LOOP_RUN = 0, LOOP_FOUND = 1, LOOP_BIG = 2, LOOP_CAPACITY = 3, LOOP_SORT = 4, LOOP_MAXCOST = 5,
+  LOOP_BLOCKS = 6, LOOP_OVERFLOW = 7
+};
+constexpr int kLoopMaxBlocks = 96;
+struct DevLoop {
+  unsigned long long* lvl_size;   // [max_cost + 1] entries of each level (0 = none)
+  unsigned long long* lvl_begin;  // [max_cost + 1]
+  unsigned long long* lvl_slab;   // [max_cost + 1]
+  unsigned long long* lvl_eval;   // [max_cost + 1] candidates evaluated
+  long long* lvl_ns;              // [max_cost + 1] level time (ns, %globaltimer)
+  Block* blocks;                  // [kLoopMaxBlocks] the current level's plan
+  LoopState* st;
+  unsigned int* bar;              // [2] grid barrier: arrivals, generation
+  unsigned long long cand_limit;  // a level with more candidates goes back to the host
+  unsigned long long entry_limit; // cache entries the loop may fill (arena / hash load)
+  unsigned long long sort_min;    // stop after a level of >= sort_min entries (0 = never)
+  unsigned long long slab_limit;  // transposed slabs the loop may fill
+  uint32_t c1, first_cost, max_cost;
+  uint32_t k_opt, k_star, k_cat, k_alt;
+  uint32_t pad;
+};
+
 // One packed launch serving many specifications: CTA group i =
 // blocks [cta_start[i], cta_start[i+1]) runs specification i with params[i].
 struct Packed {

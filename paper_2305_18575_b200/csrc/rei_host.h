@@ -36,6 +36,8 @@ int launch_union(int W32, const LevelParams& p, cudaStream_t st);
 int launch_transpose(int W32, const uint32_t* arena, uint64_t base, uint64_t count, uint32_t* tarena,
                      uint64_t slab_base, cudaStream_t st);
 int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, cudaStream_t st);
+// Device-resident loop over the small levels (DevLoop); 0 = not launched.
+int launch_level_loop(int W32, const LevelParams& p, const DevLoop& d, cudaStream_t st);
 // Packed launches (f4, rei_solve_packed): one grid, CTA group i runs pk.params[i]
 // (W32 in {1, 2} and <= 15 proper splits per word; maxk_class = 1, 3, 7 or 15).
 int packable(int W32, int maxk);
@@ -60,7 +62,7 @@ bool merge_level(int W32, const uint32_t* g_cs, const unsigned long long* g_bp, 
 void free_merge_scratch(MergeScratch& s);
 // Reorder a finished one-word (bitmap-mode) level by bitmap position, in place.
 bool sort_level(uint32_t n, uint32_t* cs, unsigned long long* bp, uint64_t m, MergeScratch& s, cudaStream_t st,
-                std::string& err, uint64_t* launches);
+                std::string& err, uint64_t* launches, bool may_skip);
 // Hash-owner exchange of a multi-rank level (exchange.cu).  Records are
 // (CS words, back-pointer as 2 words), 4 * (W32 + 2) bytes each.
 struct XScratch {

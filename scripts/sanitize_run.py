@@ -11,7 +11,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 import specgen  # noqa: E402
-from paper_2305_18575_b200 import Solver, solve_batch, solve_group  # noqa: E402
+from paper_2305_18575_b200 import Solver, solve_batch, solve_group, solve_packed  # noqa: E402
 
 CASES = [
     (specgen.C1_TOY, 12, {}),                                       # bitmap, fast kernels
@@ -33,6 +33,9 @@ def main():
     print("group", g.status, g.cost)
     rs = solve_batch([Solver.from_spec(specgen.gen_type1("01", 4, 5, 5, s), device=0) for s in range(4)], 20, 4)
     print("batch", [r.cost for r in rs])
+    specs = specgen.suite_f4(12)
+    rp, _ = solve_packed([Solver.from_spec(sp, device=0, small_cache=True) for sp in specs], 60)
+    print("packed", [r.cost for r in rp])
 
 
 if __name__ == "__main__":

@@ -133,18 +133,28 @@ def compare_search(sp, K, error=None):
     return o, g, ro, rg
 
 
+# The small levels of a search run in the device level loop (k_level_loop) by
+# default; "host" runs every level through the host loop and the level kernels
+# (REI_NO_DEVICE_LOOP), so both paths are held to the oracle.
+@pytest.fixture(params=["device_loop", "host_loop"])
+def loop_mode(request, monkeypatch):
+    if request.param == "host_loop":
+        monkeypatch.setenv("REI_NO_DEVICE_LOOP", "1")
+    return request.param
+
+
 @pytest.mark.parametrize("sp,K", SMALL, ids=ids(SMALL))
-def test_search_parity_small(sp, K):
+def test_search_parity_small(sp, K, loop_mode):
     compare_search(sp, K)
 
 
 @pytest.mark.parametrize("sp,K", RANDOM_W1, ids=ids(RANDOM_W1))
-def test_search_parity_random_w1(sp, K):
+def test_search_parity_random_w1(sp, K, loop_mode):
     compare_search(sp, K)
 
 
 @pytest.mark.parametrize("sp,K", W2, ids=ids(W2))
-def test_search_parity_w2(sp, K):
+def test_search_parity_w2(sp, K, loop_mode):
     compare_search(sp, K)
 
 
@@ -249,14 +259,14 @@ def test_long_words_use_generic_kernel(sp):
 
 
 @pytest.mark.parametrize("pct", [50, 45, 40, 35, 25, 20, 15])
-def test_allowed_error_parity(pct):
+def test_allowed_error_parity(pct, loop_mode):
     # Section 5 table rows, REI with allowed error.
     compare_search(specgen.TABLE1_ROW1, 30, error=(pct, 100))
 
 
 @pytest.mark.parametrize("sp,K", SMALL[:3] + RANDOM_W1[:4] + W2[:2] + W4[:1],
                          ids=ids(SMALL[:3] + RANDOM_W1[:4] + W2[:2] + W4[:1]))
-def test_early_exit_mode(sp, K):
+def test_early_exit_mode(sp, K, loop_mode):
     # default mode stops inside level c*: same c*, same complete levels, precise regex
     o = oracle.Oracle.from_spec(sp)
     ro = o.solve(K)
@@ -356,7 +366,7 @@ def test_table1_row1_full_vs_golden():
 
 @pytest.mark.parametrize("cap", [40, 80, 120, 160, 200, 300])
 @pytest.mark.parametrize("otf", [True, False])
-def test_onthefly_parity(cap, otf):
+def test_onthefly_parity(cap, otf, loop_mode):
     # f2: the same cache cap on both sides -> same outcome, same last
     # checked level, same cached level sets below the first OnTheFly level
     sp = specgen.C1_TOY.with_costs((1, 3, 3, 1, 3))
