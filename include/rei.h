@@ -67,6 +67,14 @@ typedef struct {
                                             x8 on demand, also in bitmap mode (which otherwise
                                             reserves all 2^|IC| entries at rei_init): many
                                             small contexts alive at once (f4)              */
+#define REI_FLAG_EXCHANGE_SELF 16u       /* a one-rank world (world_size 1 + nccl_unique_id)
+                                            that still runs every step of the multi-GPU level
+                                            exchange of SURVEY 8(e): redundant small levels with
+                                            their canonical sort, staged levels bucketed by hash
+                                            owner, grouped ncclSend/ncclRecv to itself, owner
+                                            dedup, ncclBroadcast all-gather of the uniques and
+                                            the control-line ncclAllGather -- the NCCL data
+                                            plane on one GPU (results equal a plain solve)  */
 
 /* Host all-gather supplied by the caller for REI_FLAG_SHARDED_CACHE across processes
  * (the binding builds it on torch.distributed): every rank passes `bytes` bytes in

@@ -107,6 +107,25 @@ __device__ __forceinline__ void load_cs(const uint32_t* __restrict__ arena, uint
   }
 }
 
+// the same through L2 only (ld.global.cg): data written earlier in the same launch by
+// other SMs (the device level loop) must not come from a stale L1 line
+template <int W>
+__device__ __forceinline__ void load_cs_cg(const uint32_t* __restrict__ arena, uint64_t idx, uint32_t (&x)[W]) {
+  const uint32_t* src = arena + idx * W;
+  if (W == 1) {
+    x[0] = __ldcg(src);
+  } else if (W == 2) {
+    const uint2 v = __ldcg(reinterpret_cast<const uint2*>(src));
+    x[0] = v.x; x[1] = v.y;
+  } else {
+#pragma unroll
+    for (int q = 0; q < W; q += 4) {
+      const uint4 v = __ldcg(reinterpret_cast<const uint4*>(src + q));
+      x[q] = v.x; x[q + 1] = v.y; x[q + 2] = v.z; x[q + 3] = v.w;
+    }
+  }
+}
+
 template <int W>
 __device__ __forceinline__ void store_cs(uint32_t* __restrict__ arena, uint64_t idx, const uint32_t (&x)[W]) {
   uint32_t* dst = arena + idx * W;
@@ -1710,7 +1729,7 @@ __global__ void k_seeds(LevelParams p, const uint32_t* seeds, int nsym) {
 }
 
 // Level c -> transposed slabs: warp per slab, T[32q + w] bit t = CS_t[32q + w].
-template <int W>
+template <int W, bool CG = false>
 __device__ __forceinline__ void transpose_body(const uint32_t* __restrict__ arena, unsigned long long base,
                                                unsigned long long count, uint32_t* __restrict__ tarena,
                                                unsigned long long slab_base, uint32_t bid, uint32_t nbid) {
@@ -1722,8 +1741,10 @@ __device__ __forceinline__ void transpose_body(const uint32_t* __restrict__ aren
   for (unsigned long long s = gw; s < nslabs; s += nw) {
     const unsigned long long e = s * 32 + lane;
     uint32_t x[W];
-    if (e < count) load_cs<W>(arena, base + e, x);
-    else {
+    if (e < count) {
+      if (CG) load_cs_cg<W>(arena, base + e, x);
+      else load_cs<W>(arena, base + e, x);
+    } else {
 #pragma unroll
       for (int q = 0; q < W; ++q) x[q] = 0;
     }
@@ -1843,6 +1864,7 @@ __device__ void loop_plan(const DevLoop& d, LevelCtl* ctl) {
   const uint32_t c_done = st.cost;
   bool transpose_done = false;
   st.tr_count = 0;
+  st.sorting = 0;
   if (c_done) {
     const unsigned long long size = *(volatile unsigned long long*)&ctl->count;
     const bool overflow = *(volatile unsigned int*)&ctl->overflow != 0;
@@ -1866,14 +1888,18 @@ __device__ void loop_plan(const DevLoop& d, LevelCtl* ctl) {
       return;
     }
     const bool sort = d.sort_min && size >= d.sort_min;
-    if (!sort) {  // transposed this round by every CTA
+    // a level to sort is ordered in place this round (the free arena after it is the
+    // scatter buffer, so it must hold the level once more), else by the host
+    const bool sort_here = sort && st.arena_used + 2 * size <= d.entry_limit;
+    st.sorting = sort_here ? 1u : 0u;
+    if (!sort || sort_here) {  // transposed this round by every CTA (after the sort)
       st.tr_base = st.arena_used;
       st.tr_count = size;
       st.tr_slab = st.slabs_used;
       st.slabs_used += (size + 31) / 32;
     }
     st.arena_used += size;
-    if (sort) {  // the host sorts it (its order must be fixed before it is an operand)
+    if (sort && !sort_here) {  // the host sorts it (its order is fixed before it is an operand)
       st.stop = LOOP_SORT;
       st.next_cost = c_done + 1;
       return;
@@ -1947,6 +1973,70 @@ __device__ void loop_plan(const DevLoop& d, LevelCtl* ctl) {
   st.next_cost = d.max_cost + 1;
 }
 
+// Order a finished one-word level in place by the top 12 bits of its bitmap position
+// (the locality order of the host's sort_level): bucket counts, one
+// exclusive scan, scatter to the free arena after the level, copy back.  Any order
+// of a level is valid (it is fixed before the level is an operand, and its
+// back-pointers travel with its entries); within a bucket the order is arbitrary.
+template <int W>
+__device__ void loop_sort(const LevelParams& p0, const DevLoop& d, unsigned long long base,
+                          unsigned long long count) {
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  const uint32_t n = p0.n;
+  auto bucket = [&](uint32_t cs) -> uint32_t {
+    const uint32_t key = n ? __brev(cs) >> (32 - n) : 0u;
+    return n > 12 ? key >> (n - 12) : key;
+  };
+  uint32_t* cs = p0.arena_out;
+  unsigned long long* bp = p0.bp;
+  const unsigned long long tmp = base + count;  // free arena / back-pointer space
+  for (unsigned long long i = tid; i < kLoopSortBuckets; i += nth) d.hist[i] = 0;
+  grid_sync(d.bar);
+  for (unsigned long long i = tid; i < count; i += nth) atomicAdd(&d.hist[bucket(__ldcg(cs + (base + i) * W))], 1u);
+  grid_sync(d.bar);
+  if (blockIdx.x == 0) {  // exclusive scan of the 4096 counts: 16 per thread
+    __shared__ unsigned int s_sum[256];
+    unsigned int v[16], t = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      v[k] = __ldcg(&d.hist[threadIdx.x * 16 + k]);
+      t += v[k];
+    }
+    s_sum[threadIdx.x] = t;
+    __syncthreads();
+    for (int off = 1; off < 256; off <<= 1) {
+      const unsigned int a = threadIdx.x >= (unsigned)off ? s_sum[threadIdx.x - off] : 0u;
+      __syncthreads();
+      s_sum[threadIdx.x] += a;
+      __syncthreads();
+    }
+    unsigned int run = s_sum[threadIdx.x] - t;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      d.hist[threadIdx.x * 16 + k] = run;
+      run += v[k];
+    }
+  }
+  grid_sync(d.bar);
+  for (unsigned long long i = tid; i < count; i += nth) {
+    uint32_t x[W];
+    load_cs_cg<W>(cs, base + i, x);
+    const unsigned long long b = __ldcg(bp + base + i);
+    const unsigned long long j = atomicAdd(&d.hist[bucket(x[0])], 1u);
+    store_cs<W>(cs, tmp + j, x);
+    bp[tmp + j] = b;
+  }
+  grid_sync(d.bar);
+  for (unsigned long long i = tid; i < count; i += nth) {
+    uint32_t x[W];
+    load_cs_cg<W>(cs, tmp + i, x);
+    store_cs<W>(cs, base + i, x);
+    bp[base + i] = __ldcg(bp + tmp + i);
+  }
+  grid_sync(d.bar);
+}
+
 template <int W>
 __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
   constexpr int NW = 32 * W;
@@ -1956,7 +2046,7 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
   __shared__ LevelParams sp;
   __shared__ Block s_blocks[kLoopMaxBlocks];
   __shared__ unsigned long long s_items, s_tr_base, s_tr_count, s_tr_slab;
-  __shared__ uint32_t s_nblocks, s_stop;
+  __shared__ uint32_t s_nblocks, s_stop, s_sorting;
   for (int i = threadIdx.x; i < (int)(p0.maxk * NW); i += blockDim.x)
     s_split[i] = p0.split[(i / NW) * kMaxNW + (i % NW)];
   for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p0.nsplit[i];
@@ -1979,11 +2069,13 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
       s_tr_base = vs->tr_base;
       s_tr_count = vs->tr_count;
       s_tr_slab = vs->tr_slab;
+      s_sorting = vs->sorting;
       sp.out_base = vs->out_base;
     }
     __syncthreads();
+    if (s_sorting) loop_sort<W>(p0, d, s_tr_base, s_tr_count);
     if (s_tr_count)
-      transpose_body<W>(p0.arena, s_tr_base, s_tr_count, const_cast<uint32_t*>(p0.tarena), s_tr_slab, blockIdx.x,
+      transpose_body<W, true>(p0.arena, s_tr_base, s_tr_count, const_cast<uint32_t*>(p0.tarena), s_tr_slab, blockIdx.x,
                         gridDim.x);
     if (s_stop != LOOP_RUN) break;
     for (int i = threadIdx.x; i < (int)(s_nblocks * sizeof(Block) / 4); i += blockDim.x)
@@ -2004,7 +2096,7 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
         const unsigned long long local = item - b.item_off;
         uint32_t x[W], y[W];
         if (b.kind == BK_Q || b.kind == BK_S) {
-          load_cs<W>(p0.arena, b.a_base + local, x);
+          load_cs_cg<W>(p0.arena, b.a_base + local, x);
           if (b.kind == BK_Q) {
 #pragma unroll
             for (int q = 0; q < W; ++q) cs[0][q] = x[q] | (q == 0 ? 1u : 0u);
@@ -2019,8 +2111,8 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
           if (b.tri && i >= j) {
             valid = false;
           } else {
-            load_cs<W>(p0.arena, b.a_base + i, x);
-            load_cs<W>(p0.arena, b.b_base + j, y);
+            load_cs_cg<W>(p0.arena, b.a_base + i, x);
+            load_cs_cg<W>(p0.arena, b.b_base + j, y);
             if (b.kind == BK_C) {
               concat_cs<W>(x, y, cs[0], p0.n, s_split, s_nsplit, NW);
             } else {

@@ -190,6 +190,7 @@ struct Ctx {
 
   // multi-rank
   int world = 1, rank = 0;
+  bool exchange_self = false;        // REI_FLAG_EXCHANGE_SELF: one rank, full exchange over NCCL
   void* nccl = nullptr;              // ncclComm_t (one process per GPU)
   bool host_xport = false;           // exchange through the caller's allgather callback
   LevelCtl* d_ctl_all = nullptr;     // [world] gathered control lines
@@ -767,7 +768,7 @@ rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
 // back-pointer ranks decode identically); *next = the level the host loop continues
 // with; *done = the search ended (a precise candidate).
 bool device_loop_ok(const Ctx* c, uint32_t max_cost) {
-  return !c->sharded && !c->otf_level && c->world == 1 && (c->mode == DEDUP_BITMAP || c->mode == DEDUP_HASH64) &&
+  return !c->sharded && !c->otf_level && c->world == 1 && !c->exchange_self && (c->mode == DEDUP_BITMAP || c->mode == DEDUP_HASH64) &&
          c->W32 <= 2 && max_cost <= 65535 && getenv("REI_NO_DEVICE_LOOP") == nullptr;
 }
 
@@ -782,7 +783,8 @@ rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, b
   const size_t off_blocks = 5 * arr;
   const size_t off_state = off_blocks + sizeof(Block) * kLoopMaxBlocks;
   const size_t off_bar = off_state + sizeof(LoopState);
-  const size_t bytes = off_bar + 64;
+  const size_t off_hist = off_bar + 64;
+  const size_t bytes = off_hist + 4 * kLoopSortBuckets;
   if (c->loop_bytes < bytes) {
     c->dfree(c->d_loop);
     host_free(c->h_loop);
@@ -826,8 +828,9 @@ rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, b
   d.blocks = reinterpret_cast<Block*>(dv + off_blocks);
   d.st = reinterpret_cast<LoopState*>(dv + off_state);
   d.bar = reinterpret_cast<unsigned int*>(dv + off_bar);
+  d.hist = reinterpret_cast<unsigned int*>(dv + off_hist);
   const char* ev = getenv("REI_DEVICE_LOOP_CAND");
-  d.cand_limit = ev ? strtoull(ev, nullptr, 10) : (1ull << 20);
+  d.cand_limit = ev ? strtoull(ev, nullptr, 10) : (1ull << 22);  // A/B: profiles/r02_sweep_loop.txt
   d.entry_limit = p.cap;
   d.slab_limit = c->slab_cap;
   d.sort_min = c->sort_levels ? (1ull << 14) : 0;
@@ -1371,7 +1374,7 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
   Ctx* c0 = g.m[0];
   const rei_costs& k = c0->costs;
   const int c1 = (int)k.sym;
-  const bool multi = g.world > 1;
+  const bool multi = g.world > 1 || c0->exchange_self;
   rei_status s;
   for (Ctx* c : g.m) reset_search(c);
   uint64_t cand = 1;  // Alg. 1 line 1: the empty regex is the first candidate (A9)
@@ -2241,7 +2244,8 @@ rei_status solve_packed(std::vector<Ctx*>& cs, uint32_t max_cost, std::vector<re
       c->result.candidates = 1;
       continue;
     }
-    if (c->tab.n == 0 || c->world > 1 || c->sharded || !packable(c->W32, c->tab.maxk) || c->otf_level) {
+    if (c->tab.n == 0 || c->world > 1 || c->exchange_self || c->sharded || !packable(c->W32, c->tab.maxk) ||
+        c->otf_level) {
       q.fallback = true;
       continue;
     }
@@ -2633,6 +2637,12 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       c->rank = opts->rank;
       // no NCCL id: the level exchange goes through the host all-gather callback
       c->host_xport = opts->nccl_unique_id == nullptr;
+    } else if (opts->flags & REI_FLAG_EXCHANGE_SELF) {
+      if (!opts->nccl_unique_id || c->sharded) {
+        g_init_error = "REI_FLAG_EXCHANGE_SELF needs an ncclUniqueId (and no sharded cache)";
+        return REI_EINVAL;
+      }
+      c->exchange_self = true;
     }
   }
   if (opts && opts->device >= 0) {
@@ -2667,7 +2677,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   phase("aux streams + small buffers");
   c->ctl = c->ctl_base;
   cudaMemsetAsync(c->tab.split, 0, sizeof(uint32_t) * kMaxSplitRows * kMaxNW, c->stream);
-  if (c->world > 1 && !c->sharded && !c->host_xport) {  // one process per GPU: the exchange runs over NCCL
+  if ((c->world > 1 || c->exchange_self) && !c->sharded && !c->host_xport) {  // one process per GPU: NCCL
     ncclUniqueId id;
     memcpy(&id, opts->nccl_unique_id, sizeof(id));
     ncclComm_t comm;

@@ -133,13 +133,14 @@ struct LoopState {
   uint32_t stop;                              // LoopStop
   uint32_t nblocks;
   uint32_t last_cost;                         // last level finished (complete or found)
-  uint32_t pad;
+  uint32_t sorting;                           // 1: order level [tr_base, +tr_count) this round
 };
 enum LoopStop : uint32_t {
   LOOP_RUN = 0, LOOP_FOUND = 1, LOOP_BIG = 2, LOOP_CAPACITY = 3, LOOP_SORT = 4, LOOP_MAXCOST = 5,
   LOOP_BLOCKS = 6, LOOP_OVERFLOW = 7
 };
 constexpr int kLoopMaxBlocks = 96;
+constexpr int kLoopSortBuckets = 4096;  // top 12 bits of the bitmap position
 struct DevLoop {
   unsigned long long* lvl_size;   // [max_cost + 1] entries of each level (0 = none)
   unsigned long long* lvl_begin;  // [max_cost + 1]
@@ -153,6 +154,7 @@ struct DevLoop {
   unsigned long long entry_limit; // cache entries the loop may fill (arena / hash load)
   unsigned long long sort_min;    // stop after a level of >= sort_min entries (0 = never)
   unsigned long long slab_limit;  // transposed slabs the loop may fill
+  unsigned int* hist;             // [kLoopSortBuckets] bucket counts / cursors of the level sort
   uint32_t c1, first_cost, max_cost;
   uint32_t k_opt, k_star, k_cat, k_alt;
   uint32_t pad;

@@ -22,6 +22,7 @@ FLAG_COMPLETE_FINAL_LEVEL = 1
 FLAG_NO_ONTHEFLY = 2
 FLAG_SHARDED_CACHE = 4
 FLAG_SMALL_CACHE = 8
+FLAG_EXCHANGE_SELF = 16
 KERNEL_CLASSES = ("precompute", "unary", "concat", "union", "transpose", "other")
 
 
@@ -223,7 +224,8 @@ class Solver:
                  mem_budget_bytes: int = 0, error: Optional[Tuple[int, int]] = None,
                  complete_final_level: bool = False, world_size: int = 1, rank: int = 0,
                  nccl_id: Optional[bytes] = None, max_entries: int = 0, onthefly: bool = True,
-                 sharded_cache: bool = False, allgather=None, small_cache: bool = False):
+                 sharded_cache: bool = False, allgather=None, small_cache: bool = False,
+                 exchange_self: bool = False):
         """world_size > 1 (one process per rank, rei_solve collective): the level
         exchange runs over NCCL with `nccl_id` (rank 0's nccl_unique_id()), or, with
         `allgather` and no nccl_id, through that host all-gather (bytes -> list of
@@ -243,7 +245,7 @@ class Solver:
             # host-staged level exchange through the caller's all-gather (e.g. gloo)
             self._allgather = c_allgather(allgather)
             opts.allgather = self._allgather
-        elif world_size > 1:
+        elif world_size > 1 or exchange_self:
             if nccl_id is None or len(nccl_id) < 128:
                 raise ValueError("world_size > 1 needs the 128-byte nccl_id from rank 0 "
                                  "(or an allgather callable for the host-staged exchange)")
@@ -260,7 +262,7 @@ class Solver:
             opts.err_num, opts.err_den = 0, 1
         opts.flags = (FLAG_COMPLETE_FINAL_LEVEL if complete_final_level else 0) | \
             (0 if onthefly else FLAG_NO_ONTHEFLY) | (FLAG_SHARDED_CACHE if sharded_cache else 0) | \
-            (FLAG_SMALL_CACHE if small_cache else 0)
+            (FLAG_SMALL_CACHE if small_cache else 0) | (FLAG_EXCHANGE_SELF if exchange_self else 0)
         opts.max_entries = int(max_entries)
         opts.world_size, opts.rank = int(world_size), int(rank)
         costs_c = _Costs(*[int(c) for c in costs])
