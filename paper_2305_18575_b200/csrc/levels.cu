@@ -992,6 +992,181 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
 }
 
 // ============================================================================
+// Wide concatenation (W32 = 4, 8; <= MAXK proper splits per word): the same Alg. 2
+// arithmetic as k_concat, reorganised so that a candidate costs a few instructions
+// per split instead of three dependent shared loads and a dozen ALU operations:
+//   * per lane and split (q, k) of its word 32q + lane, the byte offset of the
+//     uniform-side word u (prefix, or suffix when A is the sliced side) is fixed for
+//     the kernel; W32 = 4 keeps them in registers, W32 = 8 in a shared table;
+//   * per uniform operand x the warp writes x's bits as all-ones / zero masks to
+//     shared memory once (M[u] = -x[u], plus a zero word that invalid splits read);
+//   * per slab the sliced-side terms t_qk = T[v] are fetched once (W32 = 4: into
+//     registers, reused by every uniform operand of the work item);
+//   * the fold is then acc_q |= t_qk & M[u_qk]: one shared load + one LOP3 per split;
+//   * G uniform operands per batch, so each lane keeps G probes in flight.
+// Variant knobs (A/B on B200, profiles/r02_ab_wide_concat.txt, REI_CONCURRENT=0 solves):
+// c3-big (W32 = 4) concat 860 ms (generic k_concat) -> 776 (hoisted constants, G = 2,
+// 2 CTAs/SM) -> 750 (constants in shared memory, 4 CTAs/SM: the kernel waits on its
+// probes -- long-scoreboard stalls 12 of 18.5 cycles per issue -- so occupancy beats
+// fewer instructions); G = 4 slower (1005-1049).  For W32 = 8 every variant was slower
+// than the generic kernel (c4-big 1194-2738 vs 875 ms), which therefore keeps W32 = 8.
+#ifndef REI_WIDE_HOIST
+#define REI_WIDE_HOIST 0
+#endif
+#ifndef REI_WIDE_G
+#define REI_WIDE_G 2
+#endif
+#ifndef REI_WIDE_MINB
+#define REI_WIDE_MINB 4
+#endif
+template <int W, int MAXK, bool SLICE_A>
+__global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : 1) k_concat_wide(LevelParams p) {
+  static_assert(W == 4 || W == 8, "wide path: four- and eight-word CSs");
+  constexpr int NW = 32 * W;
+  // (MAXK 15: 120 registers of constants spill)
+  constexpr bool HOIST = REI_WIDE_HOIST && (W == 4 && MAXK <= 9);
+  constexpr int G = REI_WIDE_G;      // uniform operands (probes per lane) per batch
+  constexpr int MW = NW + 1;         // mask words per operand (+ the zero word)
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
+  uint32_t* s_cu = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);  // [MAXK][NW] uniform-side byte offsets
+  uint32_t* s_cv = s_cu + MAXK * NW;                                    // [MAXK][NW] sliced-side word index
+  uint32_t* s_warp = s_cv + MAXK * NW;                                  // [kWarps][NW + G * MW]
+  for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
+    reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  for (int i = threadIdx.x; i < MAXK * NW; i += blockDim.x) {
+    const uint32_t k = i / NW, w = i % NW;
+    const bool ok = w < p.n && k < p.nsplit[w];
+    const uint32_t sp = ok ? p.split[(size_t)k * kMaxNW + w] : 0u;
+    const uint32_t u = SLICE_A ? (sp & 0xffffu) : (sp >> 16);  // uniform side
+    const uint32_t v = SLICE_A ? (sp >> 16) : (sp & 0xffffu);  // sliced side
+    s_cu[i] = (ok ? u : (uint32_t)NW) * 4u;  // an invalid split reads the zero mask word
+    s_cv[i] = ok ? v : 0u;
+  }
+  __syncthreads();
+
+  const uint32_t lane = lane_id();
+  const uint32_t warp = threadIdx.x >> 5;
+  uint32_t* myT = s_warp + warp * (NW + G * MW);
+  uint32_t* myM = myT + NW;
+  if (lane == 0) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) myM[g * MW + NW] = 0u;
+  }
+  const uint32_t rows = (p.n + 31) / 32;  // live CS rows (warp-uniform)
+  uint32_t kq[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    const uint32_t w = q * 32 + lane;
+    kq[q] = __reduce_max_sync(kFull, w < p.n ? p.nsplit[w] : 0u);
+  }
+  uint32_t cu[HOIST ? W : 1][HOIST ? MAXK : 1];
+  if constexpr (HOIST) {
+#pragma unroll
+    for (int q = 0; q < W; ++q)
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k) cu[q][k] = s_cu[k * NW + q * 32 + lane];
+  }
+  const unsigned char* mbytes = reinterpret_cast<const unsigned char*>(myM);
+  auto ldm = [&](uint32_t off) {  // one mask word at byte offset `off` of the warp's masks
+    return *reinterpret_cast<const uint32_t*>(mbytes + off);
+  };
+
+  const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + warp;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+  for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
+    if (found_and_stop(p)) break;
+    const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
+    const unsigned long long local = item - blk.item_off;
+    const unsigned long long ut = local / blk.s_tiles, st = local % blk.s_tiles;
+    const unsigned long long nu = SLICE_A ? blk.nb : blk.na;
+    const unsigned long long ns = SLICE_A ? blk.na : blk.nb;
+    const unsigned long long u_base = SLICE_A ? blk.b_base : blk.a_base;
+    const unsigned long long slab_base = SLICE_A ? blk.a_slab : blk.b_slab;
+    const unsigned long long u0 = ut * blk.tu, u1 = min(u0 + blk.tu, nu);
+    const unsigned long long nslabs = (ns + 31) / 32;
+    const unsigned long long s0 = st * blk.ts, s1 = min(s0 + blk.ts, nslabs);
+    const unsigned long long cand_off = blk.cand_off, nb = blk.nb;
+    uint32_t evaluated = 0;
+
+    for (unsigned long long s = s0; s < s1; ++s) {
+      uint32_t T[W];
+#pragma unroll
+      for (int q = 0; q < W; ++q) T[q] = (uint32_t)q < rows ? p.tarena[(slab_base + s) * NW + q * 32 + lane] : 0u;
+      __syncwarp();
+#pragma unroll
+      for (int q = 0; q < W; ++q) myT[q * 32 + lane] = T[q];
+      __syncwarp();
+      const uint32_t Teps = __shfl_sync(kFull, T[0], 0);
+      uint32_t t[HOIST ? W : 1][HOIST ? MAXK : 1];
+      if constexpr (HOIST) {
+#pragma unroll
+        for (int q = 0; q < W; ++q)
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            t[q][k] = ((uint32_t)q < rows && (uint32_t)k < kq[q]) ? myT[s_cv[k * NW + q * 32 + lane]] : 0u;
+      }
+      const unsigned long long sj = s * 32 + lane;  // this lane's sliced operand
+      const bool lane_ok = sj < ns;
+
+      for (unsigned long long u = u0; u < u1; u += G) {
+        uint32_t cs[G][W], x[G][W];
+        bool valid[G], skip[G];
+        // the G operands' bits as masks in shared memory
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const bool active = u + g < u1;
+          if (active) load_cs<W>(p.arena, u_base + u + g, x[g]);
+          else {
+#pragma unroll
+            for (int q = 0; q < W; ++q) x[g][q] = 0u;
+          }
+#pragma unroll
+          for (int q = 0; q < W; ++q)
+            if ((uint32_t)q < rows) myM[g * MW + q * 32 + lane] = 0u - ((x[g][q] >> lane) & 1u);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const uint32_t xe = 0u - (x[g][0] & 1u);
+          uint32_t acc[W];
+#pragma unroll
+          for (int q = 0; q < W; ++q) {
+            if ((uint32_t)q >= rows) { acc[q] = 0u; continue; }
+            const uint32_t xw = 0u - ((x[g][q] >> lane) & 1u);
+            uint32_t a = (xe & T[q]) | (xw & Teps);
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k) {
+              if ((uint32_t)k >= kq[q]) break;  // warp-uniform
+              if constexpr (HOIST) {
+                a |= t[q][k] & ldm(cu[q][k] + g * MW * 4);
+              } else {
+                const uint32_t c_u = s_cu[k * NW + q * 32 + lane];
+                const uint32_t tv = myT[s_cv[k * NW + q * 32 + lane]];
+                a |= tv & ldm(c_u + g * MW * 4);
+              }
+            }
+            acc[q] = a;
+          }
+#pragma unroll
+          for (int q = 0; q < W; ++q) cs[g][q] = (uint32_t)q < rows ? transpose32(acc[q], lane) : 0u;
+          valid[g] = (u + g < u1) && lane_ok;
+          skip[g] = cs_equal<W>(cs[g], x[g]);  // equals a cached operand: old
+          evaluated += valid[g] ? 1u : 0u;
+        }
+        process_batch<W, G>(p, cs, valid, skip, [&](int g) {
+          const unsigned long long ui = u + g;
+          return cand_off + (SLICE_A ? sj * nb + ui : ui * nb + sj);
+        });
+      }
+    }
+    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
+    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
+  }
+}
+
+// ============================================================================
 // Concatenation fast path for W32 <= 2 (|IC| <= 64) and words with <= MAXK proper
 // splits.  Same arithmetic as k_concat, reorganised for instruction-level
 // parallelism:
@@ -2227,6 +2402,19 @@ size_t pair_smem(const LevelParams& p, int W) {
 // Concat grids span this many waves of resident CTAs (REI_CONCAT_WAVES, default 16; 1 =
 // persistent): with more than one, CTAs retire during the level and the union kernel of
 // a concurrent level (higher stream priority) gets SMs even when concat reached them first.
+int concat_waves();
+template <int W, int MAXK, bool SA>
+int launch_concat_wide_k(const LevelParams& p, cudaStream_t st) {
+  const size_t smem = p.nblocks * sizeof(Block) + (size_t)2 * MAXK * 32 * W * 4 +
+                      (size_t)kWarps * (32 * W + REI_WIDE_G * (32 * W + 1)) * 4;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_concat_wide<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_for(k_concat_wide<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin,
+                            concat_waves());
+  k_concat_wide<W, MAXK, SA><<<grid, kWarps * 32, smem, st>>>(p);
+  return 1;
+}
+
 int concat_waves() {
   const char* e = getenv("REI_CONCAT_WAVES");
   return e ? std::max(1, atoi(e)) : 16;
@@ -2278,6 +2466,15 @@ int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
   if constexpr (W <= 2) {
     if (p.maxk <= 15 && !getenv("REI_GENERIC_CONCAT"))
       return slice_a ? launch_concat_fast_k<W, true>(p, st) : launch_concat_fast_k<W, false>(p, st);
+  }
+  if constexpr (W == 4 || W == 8) {
+    // W32 = 8 stays on the generic kernel (A/B above); REI_WIDE_CONCAT8=1 selects this one
+    static const bool wide8 = getenv("REI_WIDE_CONCAT8") != nullptr;
+    if (p.maxk <= 15 && !getenv("REI_GENERIC_CONCAT") && (W == 4 || wide8)) {
+      if (p.maxk <= 9)
+        return slice_a ? launch_concat_wide_k<W, 9, true>(p, st) : launch_concat_wide_k<W, 9, false>(p, st);
+      return slice_a ? launch_concat_wide_k<W, 15, true>(p, st) : launch_concat_wide_k<W, 15, false>(p, st);
+    }
   }
   return launch_concat_generic<W, false>(p, st);
 }
