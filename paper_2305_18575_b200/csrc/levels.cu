@@ -189,8 +189,10 @@ __device__ bool insert_indexed(const S& p, const uint32_t (&cs)[W], unsigned lon
   const uint32_t tent = do_append ? tent_of(p) : 0u;
   unsigned long long s = h & p.dedup.mask;
   for (int probe = 0; probe < kMaxProbe; ++probe) {
-    // the level already overflowed: it will be redone after growth -- stop inserting
-    if (do_append && *(volatile unsigned int*)&p.ctl->overflow) return false;
+    // the level already overflowed: it will be redone after growth -- stop inserting.
+    // Checked every 16th probe only: the control line is one L2 round trip that would
+    // otherwise sit on every probe step's critical path
+    if (do_append && (probe & 15) == 15 && *(volatile unsigned int*)&p.ctl->overflow) return false;
     unsigned long long v = *(volatile unsigned long long*)&p.dedup.table[s];
     if (v == 0) {
       const unsigned long long lock = ((unsigned long long)fp << 32) | kLocked;
@@ -248,7 +250,8 @@ __device__ __forceinline__ bool insert_hash64(const S& p, unsigned long long key
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     if (v == key) return false;
     // the level already overflowed: it will be redone after growth -- stop inserting
-    if (*(volatile unsigned int*)&p.ctl->overflow) return false;
+    // (every 16th probe: see insert_indexed)
+    if ((probe & 15) == 15 && *(volatile unsigned int*)&p.ctl->overflow) return false;
     if (v == kEmpty64) {
       const unsigned long long old = atomicCAS(&p.dedup.table[s], kEmpty64, key);
       if (old == kEmpty64) return true;
@@ -314,8 +317,8 @@ __device__ bool insert_inline(const S& p, const unsigned long long (&k)[W / 2], 
   constexpr int U = W / 2;  // u64 words per slot
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     unsigned long long* slot = p.dedup.table + s * U;
+    if ((probe & 15) == 15 && *(volatile unsigned int*)&p.ctl->overflow) return false;  // see insert_indexed
     if (v0 == ~0ull && v1 == ~0ull) {  // empty: claim it
-      if (*(volatile unsigned int*)&p.ctl->overflow) return false;
       unsigned long long o0, o1;
       cas16(slot, ~0ull, ~0ull, k[0], (W == 8) ? (k[1] | kPend) : k[1], o0, o1);
       if (o0 == ~0ull && o1 == ~0ull) {
