@@ -38,7 +38,10 @@ namespace {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarps = 8;  // warps per CTA of the pair kernels
 // groups per lane batch (independent probes in flight); wide CSs trade MLP for registers
-template <int W> struct Batch { static constexpr int G = (W <= 2) ? 8 : (W == 4 ? 2 : 1); };
+#ifndef REI_BATCH8
+#define REI_BATCH8 1
+#endif
+template <int W> struct Batch { static constexpr int G = (W <= 2) ? 8 : (W == 4 ? 2 : (W == 8 ? REI_BATCH8 : 1)); };
 constexpr unsigned long long kEmpty64 = ~0ull;
 constexpr uint32_t kLocked = 0xffffffffu;
 constexpr int kMaxProbe = 1 << 12;  // at load <= 1/2 a longer chain means the table is full
@@ -272,6 +275,12 @@ __device__ __forceinline__ bool insert_hash64(const S& p, unsigned long long key
 // never all ones); the owner then stores the low half and clears the pending bit.
 // Readers that match the high half wait for the pending bit, then compare the low half.
 constexpr unsigned long long kPend = 1ull << 62;
+// (A/B on B200, profiles/r02_ab_w8_probe.txt: reading the low half with the head for a
+// plain-load hit test cost more than the ordered read it saves -- c4-big concat 886 ->
+// 967 ms -- and a second batch group per lane doubled the eight-word concat time)
+#ifndef REI_LOW_HINT
+#define REI_LOW_HINT 0
+#endif
 
 __device__ __forceinline__ void ld16(const unsigned long long* a, unsigned long long& x, unsigned long long& y) {
   const ulonglong2 v = *reinterpret_cast<const ulonglong2*>(a);
@@ -311,9 +320,14 @@ __device__ __forceinline__ void inline_key(const uint32_t (&cs)[W], unsigned lon
 }
 
 // Resolve the insert of an inline key whose slot `s` head (16 B) is already loaded.
+// W32 = 8: (l0, l1) = the slot's low half read together with its head by a plain
+// load (same 32-byte sector) when have_low; a low half only ever goes from empty to its
+// final value within a launch, so an equal one proves a hit and anything else falls
+// back to the ordered (volatile) read below.
 template <int W, class S>
 __device__ bool insert_inline(const S& p, const unsigned long long (&k)[W / 2], unsigned long long s,
-                              unsigned long long v0, unsigned long long v1) {
+                              unsigned long long v0, unsigned long long v1, unsigned long long l0 = 0,
+                              unsigned long long l1 = 0, bool have_low = false) {
   constexpr int U = W / 2;  // u64 words per slot
   for (int probe = 0; probe < kMaxProbe; ++probe) {
     unsigned long long* slot = p.dedup.table + s * U;
@@ -337,6 +351,7 @@ __device__ bool insert_inline(const S& p, const unsigned long long (&k)[W / 2], 
       if (W == 4) return false;
       // a low half equal to the key's is the key, whatever order the loads took (a slot
       // only ever goes from empty to its final value): the common hit needs no fence
+      if (have_low && l0 == k[U > 2 ? 2 : 0] && l1 == k[U > 2 ? 3 : 1]) return false;
       unsigned long long w0, w1;
       ld16v(slot + 2, w0, w1);
       if (w0 == k[U > 2 ? 2 : 0] && w1 == k[U > 2 ? 3 : 1]) return false;
@@ -351,6 +366,10 @@ __device__ bool insert_inline(const S& p, const unsigned long long (&k)[W / 2], 
     }
     s = (s + 1) & p.dedup.mask;
     ld16(p.dedup.table + s * U, v0, v1);
+    if (W == 8 && REI_LOW_HINT) {
+      ld16(p.dedup.table + s * U + 2, l0, l1);
+      have_low = true;
+    }
   }
   p.ctl->overflow = 1;
   return false;
@@ -660,21 +679,26 @@ __device__ __forceinline__ void process_batch(const LevelParams& p, uint32_t (&c
   } else if (p.dedup.mode == DEDUP_HASHIN) {
     if constexpr (W == 4 || W == 8) {
       // inline wide keys: the G slot heads are loaded before any is resolved
-      unsigned long long key[G][W / 2], slot[G], v0[G], v1[G];
+      unsigned long long key[G][W / 2], slot[G], v0[G], v1[G], l0[G], l1[G];
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         inline_key<W>(cs[g], key[g]);
         slot[g] = hash_cs<W>(cs[g]) & p.dedup.mask;
         v0[g] = key[g][0];
         v1[g] = key[g][1];
-        if (valid[g] && !skip[g]) ld16(p.dedup.table + slot[g] * (W / 2), v0[g], v1[g]);
+        l0[g] = l1[g] = 0;
+        if (valid[g] && !skip[g]) {
+          ld16(p.dedup.table + slot[g] * (W / 2), v0[g], v1[g]);
+          if (W == 8 && REI_LOW_HINT) ld16(p.dedup.table + slot[g] * (W / 2) + 2, l0[g], l1[g]);  // same sector
+        }
       }
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         if (!valid[g] || skip[g]) continue;
         // W32 = 4: a head equal to the key is a hit without leaving the register file
         if (W == 4 && v0[g] == key[g][0] && v1[g] == key[g][1]) continue;
-        if (insert_inline<W>(p, key[g], slot[g], v0[g], v1[g])) on_new<W>(p, cs[g], rank_of, g);
+        if (insert_inline<W>(p, key[g], slot[g], v0[g], v1[g], l0[g], l1[g], W == 8 && REI_LOW_HINT))
+          on_new<W>(p, cs[g], rank_of, g);
       }
     }
   } else {
