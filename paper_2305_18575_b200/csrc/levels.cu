@@ -1035,8 +1035,8 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
 // c3-big (W32 = 4) concat 860 ms (generic k_concat) -> 776 (hoisted constants, G = 2,
 // 2 CTAs/SM) -> 750 (constants in shared memory, 4 CTAs/SM: the kernel waits on its
 // probes -- long-scoreboard stalls 12 of 18.5 cycles per issue -- so occupancy beats
-// fewer instructions); G = 4 slower (1005-1049).  For W32 = 8 every variant was slower
-// than the generic kernel (c4-big 1194-2738 vs 875 ms), which therefore keeps W32 = 8.
+// fewer instructions); G = 4 slower (1005-1049).  W32 = 8: one operand per batch (two
+// doubled the time: fewer resident warps) at 4 CTAs/SM.
 #ifndef REI_WIDE_HOIST
 #define REI_WIDE_HOIST 0
 #endif
@@ -1046,13 +1046,21 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
 #ifndef REI_WIDE_MINB
 #define REI_WIDE_MINB 4
 #endif
+#ifndef REI_WIDE_G8
+#define REI_WIDE_G8 1
+#endif
+// eight-word CSs (A/B, profiles/r02_ab_w8_wide.txt, c4-big concat): generic k_concat 887
+// ms; this kernel with one operand per batch at 3 CTAs/SM 827, at 4 CTAs/SM 750 ms
+#ifndef REI_WIDE_MINB8
+#define REI_WIDE_MINB8 4
+#endif
 template <int W, int MAXK, bool SLICE_A>
-__global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : 1) k_concat_wide(LevelParams p) {
+__global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : REI_WIDE_MINB8) k_concat_wide(LevelParams p) {
   static_assert(W == 4 || W == 8, "wide path: four- and eight-word CSs");
   constexpr int NW = 32 * W;
   // (MAXK 15: 120 registers of constants spill)
   constexpr bool HOIST = REI_WIDE_HOIST && (W == 4 && MAXK <= 9);
-  constexpr int G = REI_WIDE_G;      // uniform operands (probes per lane) per batch
+  constexpr int G = W == 4 ? REI_WIDE_G : REI_WIDE_G8;  // uniform operands (probes per lane) per batch
   constexpr int MW = NW + 1;         // mask words per operand (+ the zero word)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
@@ -2433,7 +2441,7 @@ int concat_waves();
 template <int W, int MAXK, bool SA>
 int launch_concat_wide_k(const LevelParams& p, cudaStream_t st) {
   const size_t smem = p.nblocks * sizeof(Block) + (size_t)2 * MAXK * 32 * W * 4 +
-                      (size_t)kWarps * (32 * W + REI_WIDE_G * (32 * W + 1)) * 4;
+                      (size_t)kWarps * (32 * W + (W == 4 ? REI_WIDE_G : REI_WIDE_G8) * (32 * W + 1)) * 4;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_concat_wide<W, MAXK, SA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_for(k_concat_wide<W, MAXK, SA>, kWarps * 32, smem, kWarps, p.total_items - p.item_begin,
@@ -2495,9 +2503,7 @@ int launch_concat_t(const LevelParams& p, bool slice_a, cudaStream_t st) {
       return slice_a ? launch_concat_fast_k<W, true>(p, st) : launch_concat_fast_k<W, false>(p, st);
   }
   if constexpr (W == 4 || W == 8) {
-    // W32 = 8 stays on the generic kernel (A/B above); REI_WIDE_CONCAT8=1 selects this one
-    static const bool wide8 = getenv("REI_WIDE_CONCAT8") != nullptr;
-    if (p.maxk <= 15 && !getenv("REI_GENERIC_CONCAT") && (W == 4 || wide8)) {
+    if (p.maxk <= 15 && !getenv("REI_GENERIC_CONCAT")) {
       if (p.maxk <= 9)
         return slice_a ? launch_concat_wide_k<W, 9, true>(p, st) : launch_concat_wide_k<W, 9, false>(p, st);
       return slice_a ? launch_concat_wide_k<W, 15, true>(p, st) : launch_concat_wide_k<W, 15, false>(p, st);
