@@ -162,8 +162,11 @@ rei_status rei_solve(void* ctx, uint32_t max_cost, rei_result* out);
 /* Per-level statistics of the last rei_solve; *n_out = number available. */
 rei_status rei_level_stats(const void* ctx, rei_level_stat* buf, size_t cap, size_t* n_out);
 
-/* Accumulated launches and device milliseconds (CUDA events on the context's stream)
- * of one kernel class since the last rei_reset_kernel_stats. */
+/* Accumulated launches and device milliseconds (CUDA events on the launching stream)
+ * of one kernel class since the last rei_reset_kernel_stats.  Per-kernel events cost
+ * host time on every launch, so a context records them only after its first
+ * rei_reset_kernel_stats (or with REI_KERNEL_EVENTS=1); before that, `ms` stays 0 and
+ * the per-level times come from one event pair per level.  Launch counts always. */
 rei_status rei_kernel_stats(const void* ctx, rei_kernel_class k, uint64_t* launches, double* ms);
 rei_status rei_reset_kernel_stats(void* ctx);
 /* Total kernel launches issued by this context (all classes). */

@@ -251,6 +251,8 @@ struct Ctx {
       if (ev_join[i]) cudaEventDestroy(ev_join[i]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    for (auto e : lvl_ev)
+      if (e) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -262,23 +264,43 @@ struct Ctx {
     }
     return ev_pool[ev_next++];
   }
+  // per-kernel CUDA events (rei_kernel_stats); off (REI_KERNEL_EVENTS=0): one event
+  // pair per level on the context's stream gives the level time
+  bool kernel_events = false;  // on after rei_reset_kernel_stats (or REI_KERNEL_EVENTS=1)
+  cudaEvent_t lvl_ev[2] = {nullptr, nullptr};
+  bool lvl_open = false;
   void begin_kernel(int cls, EventPair& ep, cudaStream_t s = nullptr) {
-    ep.a = next_event();
-    ep.b = next_event();
     ep.cls = cls;
     ep.s = s ? s : stream;
+    if (!kernel_events) return;
+    ep.a = next_event();
+    ep.b = next_event();
     cudaEventRecord(ep.a, ep.s);
   }
   void end_kernel(EventPair& ep, int n) {
-    cudaEventRecord(ep.b, ep.s);
     launches += n;
     k_launches[ep.cls] += n;
+    if (!kernel_events) return;
+    cudaEventRecord(ep.b, ep.s);
     pending.push_back(ep);
+  }
+  void level_mark(int i) {  // 0 before a level's first launch, 1 after its join
+    if (kernel_events) return;
+    if (!lvl_ev[i]) cudaEventCreate(&lvl_ev[i]);
+    cudaEventRecord(lvl_ev[i], stream);
+    lvl_open = true;
   }
   // after a stream sync: fold the pending event pairs into the per-class totals
   // level_ms = the wall span of the pending launches (first start to last end): a
   // level's kernels may overlap on the auxiliary streams, so their sum would overcount
   void collect_events(double* level_ms) {
+    if (!kernel_events) {
+      float ms = 0;
+      if (lvl_open && lvl_ev[0] && lvl_ev[1]) cudaEventElapsedTime(&ms, lvl_ev[0], lvl_ev[1]);
+      lvl_open = false;
+      if (level_ms) *level_ms = ms;
+      return;
+    }
     float lo = 0, hi = 0;
     for (auto& ep : pending) {
       float ms = 0, a = 0, b = 0;
@@ -1293,6 +1315,7 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     // fill the SMs as union CTAs retire (an early exit at c* is met in union first)
     sn = c->stream;
   }
+  c->level_mark(0);
   if (conc >= 1) {
     CUDA_OK(c, cudaEventRecord(c->ev_fork, c->stream));
     for (int i = 0; i < conc; ++i) CUDA_OK(c, cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0));
@@ -1345,6 +1368,7 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
       CUDA_OK(c, cudaStreamWaitEvent(c->stream, c->ev_join[i], 0));
     }
   }
+  c->level_mark(1);
   CUDA_OK(c, cudaGetLastError());
   return REI_OK;
 }
@@ -2721,6 +2745,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   // B200, full final level: Table 1 row 1 67.5 -> 63.6 ms, row 8 neutral; a full 25-bit
   // sort cut the kernels as much but cost more).  REI_NO_LEVEL_SORT disables it.
   c->sort_levels = c->mode == DEDUP_BITMAP && !c->sharded && getenv("REI_NO_LEVEL_SORT") == nullptr;
+  if (const char* ke = getenv("REI_KERNEL_EVENTS")) c->kernel_events = atoi(ke) != 0;
   // Launch order of a level's binary kernels (REI_UNION_FIRST=0/1 overrides).  With the
   // bitmap dedup the union kernel goes first: the early exit at c* then no longer waits
   // for the union CTAs to get SMs behind a full concat grid (A/B on B200, 15 interleaved
@@ -2833,6 +2858,7 @@ rei_status rei_kernel_stats(const void* ctx, rei_kernel_class k, uint64_t* launc
 rei_status rei_reset_kernel_stats(void* ctx) {
   if (!ctx) return REI_EINVAL;
   Ctx* c = static_cast<Ctx*>(ctx);
+  c->kernel_events = true;  // per-kernel CUDA events from now on (a few us of host time per launch)
   for (int i = 0; i < REI_K_COUNT; ++i) { c->k_launches[i] = 0; c->k_ms[i] = 0; }
   c->launches = 0;
   return REI_OK;
