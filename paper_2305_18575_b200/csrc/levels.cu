@@ -1607,7 +1607,10 @@ __device__ __forceinline__ void union_body(const LevelParams& p, uint32_t bid, u
 
 // (minB: W = 2 keeps 2 CTAs per SM)
 template <int W, bool SH = false>
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : 1)) k_union(LevelParams p) {
+#ifndef REI_UNION_MINBW
+#define REI_UNION_MINBW 1
+#endif
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : REI_UNION_MINBW)) k_union(LevelParams p) {
   union_body<W, SH>(p, blockIdx.x, gridDim.x);
 }
 template <int W>
