@@ -111,6 +111,7 @@ struct EventPair {
 
 struct Ctx {
   int device = 0;
+  int sms = 148;  // multiprocessors of `device` (work-item sizing)
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   std::string alphabet;
@@ -187,6 +188,20 @@ struct Ctx {
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr;
   cudaEvent_t ev_join[3] = {nullptr, nullptr, nullptr};
+  // post-level work (the finished level's sort + transpose) on its own stream, so that
+  // the next level's concatenation / union kernels -- which never read the level just
+  // finished -- start without waiting for it; anything that reads that level waits
+  cudaStream_t post = nullptr;
+  cudaEvent_t ev_level_done = nullptr, ev_post = nullptr;
+  bool post_pending = false;
+  int post_level = 0;
+  void wait_post(cudaStream_t s) {
+    if (post_pending) cudaStreamWaitEvent(s, ev_post, 0);
+  }
+  void join_post() {  // the context's stream (and everything after it) sees the post work
+    wait_post(stream);
+    post_pending = false;
+  }
 
   // multi-rank
   int world = 1, rank = 0;
@@ -230,6 +245,7 @@ struct Ctx {
   }
 
   ~Ctx() {
+    if (post) cudaStreamSynchronize(post);
     if (stream) cudaStreamSynchronize(stream);
     for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
     for (void* q : {(void*)arena, (void*)bp, (void*)tarena, (void*)bitmap, (void*)table, (void*)special,
@@ -251,6 +267,9 @@ struct Ctx {
       if (ev_join[i]) cudaEventDestroy(ev_join[i]);
     }
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (post) cudaStreamDestroy(post);
+    if (ev_level_done) cudaEventDestroy(ev_level_done);
+    if (ev_post) cudaEventDestroy(ev_post);
     for (auto e : lvl_ev)
       if (e) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
@@ -578,11 +597,11 @@ void plan_level(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std::v
   ncat = 0;
   // candidates per work item: large items amortise the per-slab set-up at deep
   // levels; small levels get small items so that ~4 items per resident warp
-  // (148 SMs x 24 warps) keep every SM busy instead of a few warps running serially
+  // (SMs x 24 warps) keep every SM busy instead of a few warps running serially
   uint64_t pairs = 0;
   for (int L = c1; L <= cost - (int)k.cat - c1; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.cat - L);
   for (int L = c1; L <= cost - (int)k.alt - L; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.alt - L);
-  const uint64_t target = std::min<uint64_t>(8192, std::max<uint64_t>(128, pairs / (148 * 24 * 4)));
+  const uint64_t target = std::min<uint64_t>(8192, std::max<uint64_t>(128, pairs / ((uint64_t)c->sms * 24 * 4)));
   auto tile_u = [&](uint64_t nu) { return std::max<uint64_t>(1, std::min<uint64_t>({64, nu, target / 32})); };
   uint64_t item_off = 0;
   for (int L = c1; L <= cost - (int)k.cat - c1; ++L) {
@@ -658,6 +677,7 @@ void renumber_items(std::vector<Block>& v) {
 }
 
 rei_status rebuild_dedup(Ctx* c, uint64_t entries) {
+  c->join_post();
   rei_status s = clear_dedup(c);
   if (s != REI_OK) return s;
   if ((s = reset_ctl(c)) != REI_OK) return s;  // a stale overflow flag would stop the inserts
@@ -715,6 +735,7 @@ uint64_t device_total_bytes(int dev) {
 
 rei_status grow(Ctx* c, uint64_t need_entries) {
   if (c->sharded) return REI_OUT_OF_MEMORY;  // peers map the buffers: fixed at rei_init
+  c->join_post();  // the copy below must see the last level's sort and transpose
   // the bitmap-mode cache already holds every one of the 2^n possible CSs: nothing to
   // grow, and no cudaMemGetInfo (0.3-70 ms on B200) for the budget (it was the 8-15 ms
   // tail of fresh-context solves of Table 1 row 1 at level 28)
@@ -772,6 +793,7 @@ rei_status grow(Ctx* c, uint64_t need_entries) {
 }
 
 rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
+  c->join_post();  // reconstruction reads back-pointers of the last sorted level
   std::string rx;
   int pr;
   if (!rebuild(c, cost, rank, rx, pr, 0)) {
@@ -1315,10 +1337,22 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     // fill the SMs as union CTAs retire (an early exit at c* is met in union first)
     sn = c->stream;
   }
+  // the previous level's sort + transpose (post stream): the unary kernel reads that
+  // level (Q / S blocks); concatenation / union blocks wait only if one of them does
+  if (c->post_pending) {
+    bool binary_reads = conc < 1;
+    for (const Block& b : cat) binary_reads |= b.a_base == c->levels.at(c->post_level).begin ||
+                                               b.b_base == c->levels.at(c->post_level).begin;
+    for (const Block& b : uni) binary_reads |= b.a_base == c->levels.at(c->post_level).begin ||
+                                               b.b_base == c->levels.at(c->post_level).begin;
+    if (binary_reads) c->join_post();
+  }
   c->level_mark(0);
   if (conc >= 1) {
     CUDA_OK(c, cudaEventRecord(c->ev_fork, c->stream));
     for (int i = 0; i < conc; ++i) CUDA_OK(c, cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0));
+    c->wait_post(su);  // su = aux[0]: the unary kernel
+    c->post_pending = false;  // the join below makes the context's stream wait for su
   }
   if (nq + ns) {
     const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
@@ -1640,23 +1674,36 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
       c->result.candidates = cand;
       c->result.last_complete_cost = (uint32_t)cost;
       if (otf_now) continue;  // nothing cached at this level
+      if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
+        if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
+      }
+      // the level's sort and transpose run on the post stream when this context has one
+      // (single rank): the next level's binary kernels start meanwhile (launch_level)
+      const bool overlap = c->post && !multi;
+      cudaStream_t ps = overlap ? c->post : c->stream;
+      if (overlap) {
+        CUDA_OK(c, cudaEventRecord(c->ev_level_done, c->stream));
+        CUDA_OK(c, cudaStreamWaitEvent(c->post, c->ev_level_done, 0));
+      }
       if (c->sort_levels && lv.size >= (1u << 14) && !redundant) {  // bitmap mode: order by bitmap position
         std::string err;
-        if (!sort_level((uint32_t)c->tab.n, c->arena + lv.begin, c->bp + lv.begin, lv.size, c->merge, c->stream,
-                        err, &c->launches, g.world == 1)) {
+        if (!sort_level((uint32_t)c->tab.n, c->arena + lv.begin, c->bp + lv.begin, lv.size, c->merge, ps, err,
+                        &c->launches, g.world == 1)) {
           c->err = err;
           return REI_ECUDA;
         }
       }
       // transposed copy of level c (the sliced-operand layout for later levels)
-      if (c->slabs_used + (lv.size + 31) / 32 > c->slab_cap) {
-        if ((s = grow(c, c->cap + 1)) != REI_OK) return s;
-      }
       EventPair et;
-      c->begin_kernel(REI_K_TRANSPOSE, et);
-      int n = launch_transpose(c->W32, c->arena, lv.begin, lv.size, c->tarena, lv.slab, c->stream);
+      c->begin_kernel(REI_K_TRANSPOSE, et, ps);
+      int n = launch_transpose(c->W32, c->arena, lv.begin, lv.size, c->tarena, lv.slab, ps);
       c->end_kernel(et, n);
       c->slabs_used += (lv.size + 31) / 32;
+      if (overlap) {
+        CUDA_OK(c, cudaEventRecord(c->ev_post, c->post));
+        c->post_pending = true;
+        c->post_level = cost;
+      }
     }
   }
   return REI_NOT_FOUND;
@@ -1829,7 +1876,7 @@ void plan_sharded(Ctx* c, int cost, LevelInfo& lv, std::vector<Block>& cat, std:
   uint64_t pairs = 0;
   for (int L = c1; L <= cost - (int)k.cat - c1; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.cat - L);
   for (int L = c1; L <= cost - (int)k.alt - L; ++L) pairs += level_size(c, L) * level_size(c, cost - (int)k.alt - L);
-  const uint64_t target = std::min<uint64_t>(8192, std::max<uint64_t>(128, pairs / (148 * 24 * 4)));
+  const uint64_t target = std::min<uint64_t>(8192, std::max<uint64_t>(128, pairs / ((uint64_t)c->sms * 24 * 4)));
   auto tile_u = [&](uint64_t nu) { return std::max<uint64_t>(1, std::min<uint64_t>({64, nu, target / 32})); };
   auto add = [&](std::vector<Block>& v, uint32_t kind, int L, int R, const Shard& a, const Shard& b, bool tri,
                  uint64_t cnt, uint64_t& item_off) {
@@ -2187,7 +2234,9 @@ rei_status solve_impl(Ctx* c, uint32_t max_cost) {
   g.nccl = c->nccl;
   g.host = c->world > 1 && c->host_xport;
   if (c->sharded && c->world > 1) return solve_sharded(g, max_cost);
-  return solve_group(g, max_cost);
+  const rei_status s = solve_group(g, max_cost);
+  c->join_post();  // later calls (level reads, the next solve) see every level in place
+  return s;
 }
 
 // ============================================================================
@@ -2415,7 +2464,7 @@ rei_status solve_packed(std::vector<Ctx*>& cs, uint32_t max_cost, std::vector<re
     size_t po = ctlp.size(), co = 0;
     struct Launch { std::tuple<int, int, int, int> key; size_t params, cta, nspec; uint32_t ctas; size_t maxnb; };
     std::vector<Launch> launches;
-    const uint32_t budget = 148u * 4u * 4u;  // CTAs per packed launch: ~4 resident per SM x 4 waves
+    const uint32_t budget = (uint32_t)cs[0]->sms * 4u * 4u;  // CTAs per packed launch: ~4 resident per SM x 4 waves
     for (auto& kv : cls) {
       auto& items = kv.second;
       uint64_t tot = 0;
@@ -2675,6 +2724,10 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
   } else {
     cudaGetDevice(&c->device);
   }
+  {
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device) == cudaSuccess && sms > 0) c->sms = sms;
+  }
   if (opts && opts->stream) {
     c->stream = (cudaStream_t)opts->stream;
   } else {
@@ -2782,6 +2835,12 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
           return fail("auxiliary stream creation failed");
       if (cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess)
         return fail("event creation failed");
+      // post-level stream (single-rank searches; REI_NO_POST_OVERLAP=1 keeps it inline)
+      if (c->world == 1 && !c->exchange_self && !c->sharded && getenv("REI_NO_POST_OVERLAP") == nullptr &&
+          (cudaStreamCreateWithPriority(&c->post, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
+           cudaEventCreateWithFlags(&c->ev_level_done, cudaEventDisableTiming) != cudaSuccess ||
+           cudaEventCreateWithFlags(&c->ev_post, cudaEventDisableTiming) != cudaSuccess))
+        return fail("post-level stream creation failed");
     }
   }
 

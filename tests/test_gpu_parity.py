@@ -426,3 +426,18 @@ def test_cached_allocator_reuse_and_release():
         g.close()
         if i == 1:
             release_cached_memory()
+
+
+# |IC| = 64 exactly: the all-ones CS (the language of (0+1)*, cost 4 under unit costs)
+# equals the empty-slot sentinel of the 64-bit-key hash set and takes its flag path
+N64 = [(specgen.gen_type1("01", 7, 5, 5, 3), 11), (specgen.gen_type1("01", 7, 4, 4, 15), 11)]
+
+
+@pytest.mark.parametrize("sp,K", N64, ids=["t1-le7-s3", "t1-le7-s15"])
+def test_ic_64_all_ones_sentinel(sp, K, loop_mode):
+    o, g, ro, rg = compare_search(sp, K)
+    assert o.n == 64
+    ones = (1 << 64) - 1
+    assert ones in g.level_cs(4) and ones in o.level_cs(4)
+    # nowhere else: the flag makes it a single cached language
+    assert sum(l.count(ones) for l in (g.level_cs(c) for c in range(1, K + 1))) == 1
