@@ -1610,7 +1610,10 @@ template <int W, bool SH = false>
 #ifndef REI_UNION_MINBW
 #define REI_UNION_MINBW 1
 #endif
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? 2 : REI_UNION_MINBW)) k_union(LevelParams p) {
+#ifndef REI_UNION_MINB2
+#define REI_UNION_MINB2 2
+#endif
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_UNION_MINB1 : (W == 2 ? REI_UNION_MINB2 : REI_UNION_MINBW)) k_union(LevelParams p) {
   union_body<W, SH>(p, blockIdx.x, gridDim.x);
 }
 template <int W>
@@ -1730,7 +1733,10 @@ __device__ __forceinline__ void unary_fast_body(const LevelParams& p, unsigned l
   const unsigned long long gwarp = ((unsigned long long)bid * blockDim.x + threadIdx.x) >> 5;
   const unsigned long long nwarps = ((unsigned long long)nbid * blockDim.x) >> 5;
   uint32_t evaluated = 0;
-  constexpr int G = 4;  // slabs per batch: G independent probes per lane in flight
+#ifndef REI_UNARY_G
+#define REI_UNARY_G 2  // A/B (profiles/r02_ab_unary_union.txt): C2 unary 31.5 (G = 4) -> 29.4 ms, G = 8 37.9
+#endif
+  constexpr int G = REI_UNARY_G;  // slabs per batch: G independent probes per lane in flight
   const unsigned long long nslab = slabs_q + slabs_s;
   for (unsigned long long it0 = gwarp * G; it0 < nslab; it0 += nwarps * G) {
    uint32_t cs[G][W];

@@ -15,6 +15,7 @@ from paper_2305_18575_b200 import Solver  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("--") else "table1-row1"
 spec, max_cost, _ = bench.WORKLOADS[name]
 s = Solver.from_spec(spec, device=0, complete_final_level="--complete" in sys.argv)
+s.reset_kernel_stats()  # per-kernel CUDA events on (include/rei.h rei_kernel_stats)
 r = s.solve(max_cost)
 print(r.status, r.cost, r.regex, r.candidates, f"{r.seconds * 1000:.2f} ms")
 for l in r.levels:
