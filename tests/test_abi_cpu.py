@@ -74,3 +74,25 @@ def test_nccl_is_resolved_at_run_time(lib):
     assert "nccl" not in deps
     a, b = nccl_unique_id(), nccl_unique_id()
     assert len(a) == 128 and a != b
+
+
+def test_binding_flags_match_header():
+    # the ctypes binding's option flags are the header's REI_FLAG_* values
+    import re
+    from paper_2305_18575_b200 import rei
+    hdr = open(os.path.join(ROOT, "include", "rei.h")).read()
+    flags = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define REI_FLAG_(\w+) (\d+)u", hdr)}
+    assert flags["EXCHANGE_SELF"] == rei.FLAG_EXCHANGE_SELF
+    for name in ("COMPLETE_FINAL_LEVEL", "NO_ONTHEFLY", "SHARDED_CACHE", "SMALL_CACHE"):
+        assert flags[name] == getattr(rei, "FLAG_" + name), name
+    assert len(set(flags.values())) == len(flags)  # distinct bits
+
+
+def test_sass_has_device_loop_and_wide_concat():
+    # the cooperative level loop and the wide concatenation kernels are in the library
+    import subprocess
+    lib_path = os.path.join(ROOT, "paper_2305_18575_b200", "librei_b200.so")
+    out = subprocess.run(["cuobjdump", "--list-elf", lib_path], capture_output=True, text=True).stdout
+    syms = subprocess.run(["cuobjdump", "-symbols", lib_path], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "k_level_loop" in syms and "k_concat_wide" in syms
