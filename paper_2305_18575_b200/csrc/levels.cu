@@ -1224,7 +1224,10 @@ __device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t 
 #ifndef REI_CONCAT_G1
 #define REI_CONCAT_G1 4
 #endif
-  constexpr int G = (W == 1) ? REI_CONCAT_G1 : 4;  // groups (probes per lane) in flight
+#ifndef REI_CONCAT_G2
+#define REI_CONCAT_G2 4
+#endif
+  constexpr int G = (W == 1) ? REI_CONCAT_G1 : REI_CONCAT_G2;  // groups (probes per lane) in flight
   // slabs per pass: keep SB * W * MAXK shuffled slab words in registers (<= 16 + W * MAXK)
 #ifdef REI_SB1  // (A/B) slabs per pass for one-word CSs
   constexpr int SB0 = (W == 1) ? REI_SB1 : ((W * MAXK <= 3) ? 4 : (W * MAXK <= 7 ? 2 : 1));
@@ -1473,7 +1476,13 @@ __device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t 
 }
 
 template <int W, int MAXK, bool SLICE_A>
-__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : 2) k_concat_fast(LevelParams p) {
+// two-word CSs (A/B on B200, profiles/r02_ab_c2_concat.txt, concat ms c2-t1-s0 /
+// c2-t2-s4): 2 CTAs/SM x 4 groups 77.8 / 333; 3 CTAs/SM (<= 85 registers) 94.2 / 436;
+// 3 CTAs/SM x 2 groups 81.1 / 377; 2 CTAs/SM x 8 groups 120.9 / 552
+#ifndef REI_CONCAT_MINB2
+#define REI_CONCAT_MINB2 2
+#endif
+__global__ void __launch_bounds__(kWarps * 32, W == 1 ? REI_CONCAT_MINB1 : REI_CONCAT_MINB2) k_concat_fast(LevelParams p) {
   concat_fast_body<W, MAXK, SLICE_A>(p, blockIdx.x, gridDim.x);
 }
 template <int W, int MAXK, bool SLICE_A>
