@@ -144,6 +144,7 @@ struct Ctx {
   LevelCtl* ctl = nullptr;       // the current level's control line (in ctl_base)
   LevelCtl* ctl_base = nullptr;  // [2]: sharded mode alternates by level parity
   LevelCtl* h_ctl = nullptr;  // pinned
+  unsigned long long* h_rb = nullptr;  // pinned: back-pointer reads of the reconstruction
   Block* d_blocks = nullptr;  // [3][kMaxBlocks]: concat (B sliced), concat (A sliced), union
   Block* h_blocks = nullptr;  // pinned
   static constexpr int kMaxBlocks = 4096;
@@ -254,6 +255,7 @@ struct Ctx {
                     (void*)d_small, (void*)d_small_all, d_loop})
       dfree(q);
     host_free(h_loop);
+    host_free(h_rb);
     host_free(h_peers);
     host_free(h_ctl);
     host_free(h_blocks);
@@ -524,16 +526,27 @@ enum { PR_UNION = 0, PR_CAT = 1, PR_ATOM = 2 };
 
 bool rebuild(Ctx* c, int cost, uint64_t rank, std::string& out, int& prec, int depth);
 
-bool rebuild_entry(Ctx* c, int cost, uint64_t idx, std::string& out, int& prec, int depth) {
+// device address of the back-pointer of entry idx of level `cost`
+const unsigned long long* bp_src(const Ctx* c, int cost, uint64_t idx) {
   const LevelInfo& lv = c->levels.at(cost);
-  unsigned long long r = 0;
-  const unsigned long long* src = c->bp + lv.begin + idx;
   if (!lv.ssize.empty()) {  // sharded cache: the entry lives in its owner's shard
     size_t o = 0;
     while (o + 1 < lv.ssize.size() && idx >= lv.soff[o] + lv.ssize[o]) ++o;
-    src = c->peers[o].bp + lv.sbegin[o] + (idx - lv.soff[o]);
+    return c->peers[o].bp + lv.sbegin[o] + (idx - lv.soff[o]);
   }
-  if (cudaMemcpy(&r, src, 8, cudaMemcpyDeviceToHost) != cudaSuccess) return false;
+  return c->bp + lv.begin + idx;
+}
+
+bool rebuild_entry(Ctx* c, int cost, uint64_t idx, std::string& out, int& prec, int depth) {
+  if (!c->h_rb && host_alloc(reinterpret_cast<void**>(&c->h_rb), 8 * 4096) != cudaSuccess) return false;
+  unsigned long long r = 0;
+  const unsigned long long* src = bp_src(c, cost, idx);
+  // one pinned 8-byte read on the context's stream (a pageable cudaMemcpy stages
+  // through a driver buffer: ~2x the round trip per node of the regex tree)
+  if (cudaMemcpyAsync(c->h_rb, src, 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+      cudaStreamSynchronize(c->stream) != cudaSuccess)
+    return false;
+  r = *c->h_rb;
   c->d2h_bytes += 8;
   return rebuild(c, cost, r, out, prec, depth + 1);
 }
@@ -792,14 +805,107 @@ rei_status grow(Ctx* c, uint64_t need_entries) {
   return s;
 }
 
+// The same printer over the whole tree, expanded breadth first: the children of every
+// node of one tree depth are cache entries whose back-pointers are read with one
+// stream synchronisation per depth (the recursive walk pays one per node).
+constexpr size_t kRebuildBatch = 4096;  // pinned back-pointer slots (c->h_rb)
+bool rebuild_batched(Ctx* c, int cost, uint64_t rank, std::string& out) {
+  struct TNode {
+    int cost;
+    uint64_t rank;
+    Node nd;
+    int child[2];
+    std::string s;
+    int prec;
+  };
+  std::vector<TNode> t;
+  t.push_back({cost, rank, Node{}, {-1, -1}, {}, 0});
+  std::vector<int> frontier = {0};
+  const rei_costs& k = c->costs;
+  while (!frontier.empty()) {
+    std::vector<int> next;
+    std::vector<const unsigned long long*> src;
+    for (int id : frontier) {
+      t[id].nd = decode_rank(c, t[id].cost, t[id].rank);
+      const Node& nd = t[id].nd;
+      if (nd.kind == 4) continue;
+      if (nd.kind > BK_U) return false;
+      int ncost[2], nch = 1;
+      uint64_t nidx[2];
+      if (nd.kind == BK_Q || nd.kind == BK_S) {
+        ncost[0] = (nd.kind == BK_Q) ? t[id].cost - (int)k.opt : t[id].cost - (int)k.star;
+        nidx[0] = nd.i;
+      } else {
+        ncost[0] = nd.L; nidx[0] = nd.i;
+        ncost[1] = nd.R; nidx[1] = nd.j;
+        nch = 2;
+      }
+      for (int q = 0; q < nch; ++q) {
+        if (t.size() > 100000) return false;
+        t[id].child[q] = (int)t.size();
+        t.push_back({ncost[q], 0, Node{}, {-1, -1}, {}, 0});
+        next.push_back(t[id].child[q]);
+        src.push_back(bp_src(c, ncost[q], nidx[q]));
+      }
+    }
+    if (next.size() > kRebuildBatch) return false;
+    for (size_t q = 0; q < src.size(); ++q)
+      if (cudaMemcpyAsync(c->h_rb + q, src[q], 8, cudaMemcpyDeviceToHost, c->stream) != cudaSuccess) return false;
+    if (!src.empty() && cudaStreamSynchronize(c->stream) != cudaSuccess) return false;
+    c->d2h_bytes += 8 * src.size();
+    for (size_t q = 0; q < next.size(); ++q) t[next[q]].rank = c->h_rb[q];
+    frontier.swap(next);
+  }
+  for (int id = (int)t.size() - 1; id >= 0; --id) {  // children were created after parents
+    TNode& n = t[id];
+    switch (n.nd.kind) {
+      case 4:
+        n.s = std::string(1, c->alphabet[n.nd.i]);
+        n.prec = PR_ATOM;
+        break;
+      case BK_Q:
+      case BK_S: {
+        std::string a = t[n.child[0]].s;
+        if (!(t[n.child[0]].prec == PR_ATOM && a.size() == 1)) a = "(" + a + ")";
+        n.s = a + (n.nd.kind == BK_Q ? "?" : "*");
+        n.prec = PR_ATOM;
+        break;
+      }
+      default: {
+        std::string l = t[n.child[0]].s, r = t[n.child[1]].s;
+        if (n.nd.kind == BK_C) {
+          if (t[n.child[0]].prec == PR_UNION) l = "(" + l + ")";
+          if (t[n.child[1]].prec == PR_UNION) r = "(" + r + ")";
+          n.s = l + r;
+          n.prec = PR_CAT;
+        } else {
+          n.s = l + "+" + r;
+          n.prec = PR_UNION;
+        }
+      }
+    }
+    if (id) t[id].s.shrink_to_fit();
+  }
+  out = t[0].s;
+  return true;
+}
+
 rei_status finish_found(Ctx* c, int cost, uint64_t rank) {
   c->join_post();  // reconstruction reads back-pointers of the last sorted level
   std::string rx;
   int pr;
-  if (!rebuild(c, cost, rank, rx, pr, 0)) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (!c->h_rb && host_alloc(reinterpret_cast<void**>(&c->h_rb), 8 * kRebuildBatch) != cudaSuccess) {
+    c->err = "pinned allocation failed";
+    return REI_ECUDA;
+  }
+  if (!rebuild_batched(c, cost, rank, rx) && !rebuild(c, cost, rank, rx, pr, 0)) {
     c->err = "regex reconstruction failed";
     return REI_ECUDA;
   }
+  if (getenv("REI_TRACE"))
+    fprintf(stderr, "[rei_solve] regex reconstruction: %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   c->regex = rx;
   c->result.cost = (uint32_t)cost;
   return REI_OK;
