@@ -2319,8 +2319,54 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
       uint32_t cs[1][W];
       bool skip = false;
       unsigned long long rank = 0;
-      if (valid) {
-        const Block& b = s_blocks[find_block(s_blocks, nb, item)];
+      // a warp whose 32 candidates are one concatenation row (the same left operand x,
+      // 32 consecutive right operands) folds them bit-sliced like k_concat: transpose the
+      // 32 y's, lane w ORs x[u] ? T[v] over the proper splits (u, v) of word w (plus the
+      // epsilon splits), transpose back -- a few instructions per candidate instead of a
+      // per-thread pass over every split of every word
+      const int bi = valid ? find_block(s_blocks, nb, item) : -1;
+      const int bi0 = __shfl_sync(kFull, bi, 0);
+      bool row = d.rows && valid && bi == bi0 && s_blocks[bi].kind == BK_C;
+      unsigned long long ri = 0, rj = 0;
+      if (row) {
+        const unsigned long long local = item - s_blocks[bi].item_off;
+        ri = local / s_blocks[bi].nb;
+        rj = local % s_blocks[bi].nb;
+      }
+      const unsigned long long ri0 = __shfl_sync(kFull, ri, 0);  // every lane (no short circuit)
+      row = __all_sync(kFull, row && ri == ri0);
+      if (row) {
+        const Block& b = s_blocks[bi];
+        uint32_t x[W], y[W], T[W], acc[W];
+        load_cs_cg<W>(p0.arena, b.a_base + ri, x);  // warp-uniform
+        load_cs_cg<W>(p0.arena, b.b_base + rj, y);
+#pragma unroll
+        for (int q = 0; q < W; ++q) T[q] = (uint32_t)q * 32 < p0.n ? transpose32(y[q], lane) : 0u;
+        const uint32_t Teps = __shfl_sync(kFull, T[0], 0);
+        const uint32_t xe = 0u - (x[0] & 1u);
+#pragma unroll
+        for (int q = 0; q < W; ++q) {
+          acc[q] = (xe & T[q]) | ((0u - ((x[q] >> lane) & 1u)) & Teps);
+          const uint32_t w = q * 32 + lane;
+          const uint32_t m = w < p0.n ? s_nsplit[w] : 0u;
+          const uint32_t km = __reduce_max_sync(kFull, m);
+          for (uint32_t k = 0; k < km; ++k) {
+            const uint32_t sp = k < m ? s_split[k * NW + w] : 0u;
+            const uint32_t u = sp >> 16, v = sp & 0xffffu;
+            uint32_t t = __shfl_sync(kFull, T[0], v & 31);
+            if (W == 2) {
+              const uint32_t t1 = __shfl_sync(kFull, T[W - 1], v & 31);
+              t = (v >> 5) ? t1 : t;
+            }
+            if (k < m && get_bit<W>(x, u)) acc[q] |= t;
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < W; ++q) cs[0][q] = (uint32_t)q * 32 < p0.n ? transpose32(acc[q], lane) : 0u;
+        rank = b.cand_off + ri * b.nb + rj;
+        skip = cs_equal<W>(cs[0], x) || cs_equal<W>(cs[0], y);
+      } else if (valid) {
+        const Block& b = s_blocks[bi];
         const unsigned long long local = item - b.item_off;
         uint32_t x[W], y[W];
         if (b.kind == BK_Q || b.kind == BK_S) {

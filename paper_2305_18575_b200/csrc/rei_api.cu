@@ -991,6 +991,7 @@ rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, b
   d.k_star = k.star;
   d.k_cat = k.cat;
   d.k_alt = k.alt;
+  d.rows = getenv("REI_LOOP_ROWS") ? (uint32_t)atoi(getenv("REI_LOOP_ROWS")) : 1u;
   EventPair ep;
   c->begin_kernel(REI_K_OTHER, ep);
   const int n = launch_level_loop(c->W32, p, d, c->stream);

@@ -157,7 +157,7 @@ struct DevLoop {
   unsigned int* hist;             // [kLoopSortBuckets] bucket counts / cursors of the level sort
   uint32_t c1, first_cost, max_cost;
   uint32_t k_opt, k_star, k_cat, k_alt;
-  uint32_t pad;
+  uint32_t rows;                  // 1: bit-sliced concatenation rows (REI_LOOP_ROWS=0 turns off)
 };
 
 // One packed launch serving many specifications: CTA group i =
