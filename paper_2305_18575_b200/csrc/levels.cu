@@ -2801,7 +2801,8 @@ int launch_level_loop(int W32, const LevelParams& p, const DevLoop& d, cudaStrea
     int occ = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_level_loop<W>, 256, smem) != cudaSuccess || occ < 1)
       return 0;
-    int grid = sm_count() * std::min(occ, 2);
+    static const int per_sm = getenv("REI_LOOP_CTAS_PER_SM") ? std::max(1, atoi(getenv("REI_LOOP_CTAS_PER_SM"))) : 4;  // A/B: 1 / 2 / 4 per SM -> loop 0.87 / 0.70 / 0.68 ms (Table 1 row 1)
+    int grid = sm_count() * std::min(occ, per_sm);
     LevelParams pp = p;
     DevLoop dd = d;
     void* args[] = {&pp, &dd};
