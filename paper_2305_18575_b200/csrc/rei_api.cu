@@ -922,12 +922,13 @@ bool device_loop_ok(const Ctx* c, uint32_t max_cost) {
          c->W32 <= 2 && max_cost <= 65535 && getenv("REI_NO_DEVICE_LOOP") == nullptr;
 }
 
-rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, bool* done) {
+rei_status device_levels(Ctx* c, uint32_t max_cost, int from_cost, int* next, uint64_t* cand, bool* done) {
   *done = false;
   const rei_costs& k = c->costs;
   const int c1 = (int)k.sym;
-  *next = c1 + 1;
-  if ((int)max_cost <= c1) return REI_OK;
+  *next = from_cost;
+  if ((int)max_cost < from_cost) return REI_OK;
+  c->join_post();  // the loop reads every finished level (sorted, transposed)
   const size_t L = (size_t)max_cost + 1;
   const size_t arr = L * 8;
   const size_t off_blocks = 5 * arr;
@@ -956,10 +957,12 @@ rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, b
   auto* h_ns = reinterpret_cast<long long*>(h_eval + L);
   auto* h_st = reinterpret_cast<LoopState*>(h + off_state);
   memset(h, 0, bytes);
-  const LevelInfo& l1 = c->levels.at(c1);
-  h_size[c1] = l1.size;
-  h_begin[c1] = l1.begin;
-  h_slab[c1] = l1.slab;
+  for (const auto& kv : c->levels) {  // every finished level (the loop may resume mid-search)
+    if (kv.first >= from_cost || kv.first > (int)max_cost) continue;
+    h_size[kv.first] = kv.second.size;
+    h_begin[kv.first] = kv.second.begin;
+    h_slab[kv.first] = kv.second.slab;
+  }
   h_st->arena_used = c->arena_used;
   h_st->slabs_used = c->slabs_used;
   h_st->found_rank = ~0ull;
@@ -985,7 +988,7 @@ rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, b
   d.slab_limit = c->slab_cap;
   d.sort_min = c->sort_levels ? (1ull << 14) : 0;
   d.c1 = (uint32_t)c1;
-  d.first_cost = (uint32_t)c1 + 1;
+  d.first_cost = (uint32_t)from_cost;
   d.max_cost = max_cost;
   d.k_opt = k.opt;
   d.k_star = k.star;
@@ -1009,10 +1012,10 @@ rei_status device_levels(Ctx* c, uint32_t max_cost, int* next, uint64_t* cand, b
   c->collect_events(&loop_ms);
   const LoopState S = *h_st;
   if (getenv("REI_TRACE"))
-    fprintf(stderr, "[rei_solve] device loop levels %d..%u stop %u next %u: %.3f ms\n", c1 + 1, S.last_cost, S.stop,
+    fprintf(stderr, "[rei_solve] device loop levels %d..%u stop %u next %u: %.3f ms\n", from_cost, S.last_cost, S.stop,
             S.next_cost, loop_ms);
   std::vector<Block> cat, uni;
-  for (int cost = c1 + 1; cost <= (int)S.last_cost; ++cost) {
+  for (int cost = from_cost; cost <= (int)S.last_cost; ++cost) {
     LevelInfo lv;
     lv.cost = cost;
     uint64_t nq, ns, ncat, nuni;
@@ -1610,11 +1613,19 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
   }
 
   int first_cost = c1 + 1;
-  if (!multi && g.m.size() == 1 && device_loop_ok(c0, max_cost)) {
+  const bool loop_ok = !multi && g.m.size() == 1 && device_loop_ok(c0, max_cost);
+  if (loop_ok) {
     bool done = false;
-    if ((s = device_levels(c0, max_cost, &first_cost, &cand, &done)) != REI_OK) return s;
+    if ((s = device_levels(c0, max_cost, c1 + 1, &first_cost, &cand, &done)) != REI_OK) return s;
     if (done) return REI_OK;
   }
+  // REI_LOOP_RESUME=1: after a big level on the host, a run of small levels goes back to
+  // the device loop (A/B on B200: Table 1 row 8, whose big levels alternate with runs
+  // of small ones, 45.0 ms either way -- a resumed launch costs about what the host
+  // round trips of the small levels it takes over do; off by default)
+  const char* lce = getenv("REI_DEVICE_LOOP_CAND");
+  const uint64_t loop_limit = lce ? strtoull(lce, nullptr, 10) : (1ull << 22);
+  const bool loop_resume = loop_ok && getenv("REI_LOOP_RESUME") != nullptr;
 
   std::vector<Block> cat, uni;
   std::vector<LevelCtl> all;
@@ -1632,6 +1643,16 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
     uint64_t nq, ns, ncat, nuni;
     plan_level(c0, cost, lv, cat, uni, nq, ns, ncat, nuni);  // identical on every rank
     if (lv.plan.empty()) continue;
+    if (loop_resume && !otf && cost > first_cost && nq + ns + ncat + nuni <= loop_limit) {
+      bool done = false;
+      int next = cost;
+      if ((s = device_levels(c0, max_cost, cost, &next, &cand, &done)) != REI_OK) return s;
+      if (done) return REI_OK;
+      if (next > cost) {  // the loop finished levels cost .. next - 1
+        cost = next - 1;
+        continue;
+      }
+    }
     if ((int)(cat.size() + uni.size()) > Ctx::kMaxBlocks) {
       c0->err = "too many operand blocks in one level";
       return REI_EINVAL;

@@ -30,7 +30,7 @@ def _need_gpu():
 
 def solve(sp, K, monkeypatch, env=None, **kw):
     from paper_2305_18575_b200 import Solver
-    for k in ("REI_NO_DEVICE_LOOP", "REI_DEVICE_LOOP_CAND"):
+    for k in ("REI_NO_DEVICE_LOOP", "REI_DEVICE_LOOP_CAND", "REI_LOOP_RESUME"):
         monkeypatch.delenv(k, raising=False)
     for k, v in (env or {}).items():
         monkeypatch.setenv(k, v)
@@ -56,9 +56,11 @@ CASES = [
 
 
 @pytest.mark.parametrize("sp,K,kw", CASES, ids=[f"{c[0].name or c[0].alphabet}-{i}" for i, c in enumerate(CASES)])
-@pytest.mark.parametrize("cand", [None, "3000"])
+@pytest.mark.parametrize("cand", [None, "3000", "3000-resume"])
 def test_device_loop_equals_host_loop(sp, K, kw, cand, monkeypatch):
-    env = {"REI_DEVICE_LOOP_CAND": cand} if cand else {}
+    env = {"REI_DEVICE_LOOP_CAND": cand.split("-")[0]} if cand else {}
+    if cand and cand.endswith("resume"):  # the loop resumes after every big host level
+        env["REI_LOOP_RESUME"] = "1"
     gd, rd = solve(sp, K, monkeypatch, env, **kw)
     gh, rh = solve(sp, K, monkeypatch, {"REI_NO_DEVICE_LOOP": "1"}, **kw)
     assert (rd.status, rd.cost) == (rh.status, rh.cost)
