@@ -870,6 +870,35 @@ __device__ __forceinline__ const LevelParams& packed_params(const Packed& pk, ui
 __device__ __forceinline__ bool found_and_stop(const LevelParams& p) {
   return p.early_exit && *(volatile unsigned long long*)&p.ctl->found_rank != ~0ull;
 }
+// Early exit inside a work item, once per slab pass (REI_SLAB_EXIT: 0 off, 1 a blocking
+// check at each pass, 2 the check of the value loaded one pass earlier).  A/B on B200
+// (profiles/r02_ab_slab_exit.txt, solve ms off / blocking / deferred): Table 1 row 1
+// 27.16 / 27.52 / 28.07, row 8 47.75 / 48.57 / 49.54, C2 145.0 / 148.2 / 151.2 -- the
+// extra reads of the control line (the level's append counter lives in it) cost more
+// than the shorter drain saves, so the check stays per work item
+#ifndef REI_SLAB_EXIT
+#define REI_SLAB_EXIT 0
+#endif
+#if REI_SLAB_EXIT == 0
+#define SLAB_EXIT(p, notfirst) false
+#elif REI_SLAB_EXIT == 1
+#define SLAB_EXIT(p, notfirst) ((notfirst) && found_and_stop(p))
+#else
+struct SlabExit {
+  unsigned long long seen = ~0ull;
+  __device__ __forceinline__ bool operator()(const LevelParams& p, bool notfirst) {
+    const bool stop = notfirst && p.early_exit && seen != ~0ull;
+    seen = *(volatile unsigned long long*)&p.ctl->found_rank;
+    return stop;
+  }
+};
+#define SLAB_EXIT(p, notfirst) slab_exit(p, notfirst)
+#endif
+#if REI_SLAB_EXIT == 2
+#define SLAB_EXIT_DECL SlabExit slab_exit;
+#else
+#define SLAB_EXIT_DECL
+#endif
 
 // ============================================================================
 // Concatenation kernel.  Dynamic shared memory: split table [maxk][NW], nsplit[NW],
@@ -924,7 +953,9 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
     const unsigned long long s0 = st * blk.ts, s1 = min(s0 + blk.ts, nslabs);
     uint32_t evaluated = 0;
 
+    SLAB_EXIT_DECL
     for (unsigned long long s = s0; s < s1; ++s) {
+      if (SLAB_EXIT(p, s != s0)) break;  // early exit per slab pass, not only per work item
       // the slab in transposed form
       uint32_t T[W];
 #pragma unroll
@@ -1124,7 +1155,9 @@ __global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : REI_WIDE
     const unsigned long long cand_off = blk.cand_off, nb = blk.nb;
     uint32_t evaluated = 0;
 
+    SLAB_EXIT_DECL
     for (unsigned long long s = s0; s < s1; ++s) {
+      if (SLAB_EXIT(p, s != s0)) break;  // early exit per slab pass, not only per work item
       uint32_t T[W];
 #pragma unroll
       for (int q = 0; q < W; ++q) T[q] = (uint32_t)q < rows ? p.tarena[(slab_base + s) * NW + q * 32 + lane] : 0u;
@@ -1330,7 +1363,9 @@ __device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t 
 
     // SB slabs per pass: their shuffled words stay in registers while every uniform
     // operand of the item is applied to them; a batch = GX uniform operands x SB slabs
+    SLAB_EXIT_DECL
     for (unsigned long long s = s0; s < s1; s += SB) {
+      if (SLAB_EXIT(p, s != s0)) break;  // early exit per slab pass, not only per work item
       uint32_t T[SB][W], Teps[SB], tk[SB][W][MAXK];
       bool lane_ok[SB];
 #pragma unroll
@@ -1554,7 +1589,9 @@ __device__ __forceinline__ void union_body(const LevelParams& p, uint32_t bid, u
 
     // G slabs per pass (one operand of the sliced level per lane and slab): each uniform
     // operand is broadcast once and applied to all G of them (a batch = G candidates)
+    SLAB_EXIT_DECL
     for (unsigned long long s = s0; s < s1; s += G) {
+      if (SLAB_EXIT(p, s != s0)) break;  // early exit per slab pass, not only per work item
       const unsigned long long s_last = min(s + G, s1) - 1;
       uint32_t y[G][W];
       bool lane_ok[G];
