@@ -37,17 +37,23 @@ struct Block {
   uint64_t tu, ts;            // uniform operands / slabs (of 32) per work item
 };
 
-// Per-level control block, reset before each level (one 64-byte line).
+// Per-level control block, reset before each level.  The flags every warp polls
+// (found_rank per work item, overflow every 16th probe step) sit on their own 128-byte
+// line, away from the counters the warps update atomically (count per append flush,
+// evaluated per work item): on one line the polls and the atomics serialise in the
+// same L2 slice.
 struct LevelCtl {
   unsigned long long found_rank;  // min rank of a precise candidate; ~0 = none
-  unsigned long long count;       // new CSs appended to the level
-  unsigned long long evaluated;   // candidates evaluated (items finished)
   unsigned int overflow;          // arena / hash capacity exceeded
   unsigned int special_seen;      // hash64 mode: the sentinel key was inserted
+  unsigned long long pad0[14];
+  unsigned long long count;       // new CSs appended to the level
+  unsigned long long evaluated;   // candidates evaluated (items finished)
   unsigned long long eval_c;      // of which by the concat kernel
   unsigned long long eval_u;      // of which by the union kernel
-  unsigned long long pad[2];
+  unsigned long long pad1[12];
 };
+static_assert(sizeof(LevelCtl) == 256, "two 128-byte lines");
 
 // DEDUP_HASHIN: the CS itself is the slot (16 B for W32 = 4, 32 B for W32 = 8), so a
 // probe that hits costs one random 32-byte sector; used when the top CS bit(s) are
