@@ -938,6 +938,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
   }
   const uint32_t rows = (p.n + 31) / 32;  // live CS rows (warp-uniform)
 
+  unsigned long long warp_eval = 0;
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
@@ -1044,8 +1045,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
       }
       if (!kShfl) __syncwarp();
     }
-    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
-    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
+    warp_eval += __reduce_add_sync(kFull, evaluated);  // one atomic per warp per launch (below)
+  }
+  if (lane_id() == 0 && warp_eval) {  // the control line's counters: once per warp, not per item
+    atomicAdd(&p.ctl->evaluated, warp_eval);
+    atomicAdd(&p.ctl->eval_c, warp_eval);
   }
 }
 
@@ -1140,6 +1144,7 @@ __global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : REI_WIDE
 
   const unsigned long long gwarp = (unsigned long long)blockIdx.x * kWarps + warp;
   const unsigned long long nwarps = (unsigned long long)gridDim.x * kWarps;
+  unsigned long long warp_eval = 0;
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
@@ -1229,8 +1234,11 @@ __global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : REI_WIDE
         });
       }
     }
-    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
-    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
+    warp_eval += __reduce_add_sync(kFull, evaluated);  // one atomic per warp per launch (below)
+  }
+  if (lane_id() == 0 && warp_eval) {  // the control line's counters: once per warp, not per item
+    atomicAdd(&p.ctl->evaluated, warp_eval);
+    atomicAdd(&p.ctl->eval_c, warp_eval);
   }
 }
 
@@ -1339,6 +1347,7 @@ __device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t 
   const unsigned long long gwarp = (unsigned long long)bid * kWarps + (threadIdx.x >> 5);
   const unsigned long long nwarps = (unsigned long long)nbid * kWarps;
 
+  unsigned long long warp_eval = 0;
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
@@ -1504,8 +1513,11 @@ __device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t 
 #pragma unroll
       for (int j = 0; j < SB; ++j) evaluated += lane_ok[j] ? nu_item : 0u;  // every operand of the item
     }
-    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
-    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_c, (unsigned long long)tot); }
+    warp_eval += __reduce_add_sync(kFull, evaluated);  // one atomic per warp per launch (below)
+  }
+  if (lane_id() == 0 && warp_eval) {  // the control line's counters: once per warp, not per item
+    atomicAdd(&p.ctl->evaluated, warp_eval);
+    atomicAdd(&p.ctl->eval_c, warp_eval);
   }
   if (W == 2) stage_flush<W>(p, stage);
 }
@@ -1559,6 +1571,7 @@ __device__ __forceinline__ void union_body(const LevelParams& p, uint32_t bid, u
     if (W <= 2) stage_init_lc<W>(stage, st_rank + kWarps * kStage);
   }
 
+  unsigned long long warp_eval = 0;
   for (unsigned long long item = p.item_begin + gwarp; item < p.total_items; item += nwarps) {
     if (found_and_stop(p)) break;
     const Block& blk = s_blocks[find_block(s_blocks, p.nblocks, item)];
@@ -1645,8 +1658,11 @@ __device__ __forceinline__ void union_body(const LevelParams& p, uint32_t bid, u
         }, kUnionStaged && W <= 2 ? &stage : nullptr);
       }
     }
-    const uint32_t tot = __reduce_add_sync(kFull, evaluated);
-    if (lane == 0 && tot) { atomicAdd(&p.ctl->evaluated, (unsigned long long)tot); atomicAdd(&p.ctl->eval_u, (unsigned long long)tot); }
+    warp_eval += __reduce_add_sync(kFull, evaluated);  // one atomic per warp per launch (below)
+  }
+  if (lane_id() == 0 && warp_eval) {  // the control line's counters: once per warp, not per item
+    atomicAdd(&p.ctl->evaluated, warp_eval);
+    atomicAdd(&p.ctl->eval_u, warp_eval);
   }
   if (kUnionStaged && W <= 2) stage_flush<W>(p, stage);
 }
