@@ -143,6 +143,11 @@ __device__ __forceinline__ void store_cs(uint32_t* __restrict__ arena, uint64_t 
   }
 }
 
+// first arena index of the level being built (device-resident for lagged levels)
+__device__ __forceinline__ unsigned long long out_base_of(const LevelParams& p) {
+  return p.out_base_dev ? __ldg(p.out_base_dev) : p.out_base;
+}
+
 // Warp-aggregated append of a new CS + back-pointer to level c.
 template <int W>
 __device__ __forceinline__ void append(const LevelParams& p, const uint32_t (&cs)[W], unsigned long long rank) {
@@ -153,7 +158,7 @@ __device__ __forceinline__ void append(const LevelParams& p, const uint32_t (&cs
   unsigned long long base = 0;
   if ((int)lane == leader) base = atomicAdd(&p.ctl->count, (unsigned long long)__popc(mask));
   base = __shfl_sync(mask, base, leader) + __popc(mask & ((1u << lane) - 1u));
-  const unsigned long long idx = p.out_base + base;
+  const unsigned long long idx = out_base_of(p) + base;
   if (idx >= p.cap) {
     p.ctl->overflow = 1;
     return;
@@ -471,7 +476,7 @@ __device__ __noinline__ void stage_flush_n(LevelCtl* ctl, uint32_t* arena_out, u
 template <int W>
 __device__ __forceinline__ void stage_flush(const LevelParams& p, WarpStage<W>& s) {
   if (s.n == 0) return;
-  stage_flush_n<W>(p.ctl, p.arena_out, p.bp, p.out_base, p.cap, s.cs, s.rank, s.n);
+  stage_flush_n<W>(p.ctl, p.arena_out, p.bp, out_base_of(p), p.cap, s.cs, s.rank, s.n);
   s.n = 0;
 }
 
@@ -2464,6 +2469,15 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
   }
 }
 
+// Lagged levels: the next level's first arena index = the previous (still unread) level's
+// first index + its count; a precise candidate or an overflow in that level makes the
+// next level's kernels exit at once (its found_rank is set; the host redoes or discards it)
+__global__ void k_next_base(const LevelCtl* __restrict__ prev, unsigned long long prev_begin,
+                            unsigned long long* __restrict__ base, LevelCtl* __restrict__ next) {
+  *base = prev_begin + prev->count;
+  if (prev->found_rank != ~0ull || prev->overflow) next->found_rank = 0ull;
+}
+
 // Device CS operations on explicit operand pairs (tests): thread per pair, direct
 // fold over the full guide table (epsilon splits + proper splits).
 template <int W>
@@ -2843,6 +2857,12 @@ int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, 
 int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const uint32_t* b, uint32_t* out,
                uint64_t count, cudaStream_t st) {
   REI_DISPATCH_W(W32, return launch_ops_t<W>(p, op, a, b, out, count, st));
+}
+
+int launch_next_base(const LevelCtl* prev, unsigned long long prev_begin, unsigned long long* base, LevelCtl* next,
+                     cudaStream_t st) {
+  k_next_base<<<1, 1, 0, st>>>(prev, prev_begin, base, next);
+  return 1;
 }
 
 // One cooperative launch of the device level loop; returns 1 (launched) or 0 (not

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -196,13 +197,23 @@ struct Ctx {
   cudaEvent_t ev_level_done = nullptr, ev_post = nullptr;
   bool post_pending = false;
   int post_level = 0;
+  std::vector<int> post_levels;  // every level whose sort / transpose is still on `post`
   void wait_post(cudaStream_t s) {
     if (post_pending) cudaStreamWaitEvent(s, ev_post, 0);
   }
   void join_post() {  // the context's stream (and everything after it) sees the post work
     wait_post(stream);
     post_pending = false;
+    post_levels.clear();
   }
+  // lagged levels (solve_lagged): device base of the level being launched, the previous
+  // (unread) level's control line and first arena index
+  unsigned long long* d_lag_base = nullptr;  // [2]
+  const LevelCtl* lag_prev_ctl = nullptr;
+  uint64_t lag_prev_begin = 0;
+  int lag_par = 0;
+  LevelCtl* h_lag = nullptr;  // pinned [2]: control lines read back without a stream sync
+  cudaEvent_t ev_lag[2] = {nullptr, nullptr};
 
   // multi-rank
   int world = 1, rank = 0;
@@ -252,10 +263,13 @@ struct Ctx {
     for (void* q : {(void*)arena, (void*)bp, (void*)tarena, (void*)bitmap, (void*)table, (void*)special,
                     (void*)ctl_base, (void*)d_blocks, (void*)d_peers, (void*)tab.split, (void*)tab.nsplit,
                     (void*)tab.word_len, (void*)tab.seeds, (void*)d_ctl_all, (void*)st_cs, (void*)st_bp,
-                    (void*)d_small, (void*)d_small_all, d_loop})
+                    (void*)d_small, (void*)d_small_all, d_loop, (void*)d_lag_base})
       dfree(q);
     host_free(h_loop);
     host_free(h_rb);
+    host_free(h_lag);
+    for (auto e : ev_lag)
+      if (e) cudaEventDestroy(e);
     host_free(h_peers);
     host_free(h_ctl);
     host_free(h_blocks);
@@ -272,8 +286,9 @@ struct Ctx {
     if (post) cudaStreamDestroy(post);
     if (ev_level_done) cudaEventDestroy(ev_level_done);
     if (ev_post) cudaEventDestroy(ev_post);
-    for (auto e : lvl_ev)
-      if (e) cudaEventDestroy(e);
+    for (auto& pr : lvl_ev_p)
+      for (auto e : pr)
+        if (e) cudaEventDestroy(e);
     if (own_stream && stream) cudaStreamDestroy(stream);
   }
 
@@ -288,8 +303,9 @@ struct Ctx {
   // per-kernel CUDA events (rei_kernel_stats); off (REI_KERNEL_EVENTS=0): one event
   // pair per level on the context's stream gives the level time
   bool kernel_events = false;  // on after rei_reset_kernel_stats (or REI_KERNEL_EVENTS=1)
-  cudaEvent_t lvl_ev[2] = {nullptr, nullptr};
-  bool lvl_open = false;
+  cudaEvent_t lvl_ev_p[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  bool lvl_open_p[2] = {false, false};
+  int ev_par = 0;  // which pair level_mark / collect_events use (lagged levels alternate)
   void begin_kernel(int cls, EventPair& ep, cudaStream_t s = nullptr) {
     ep.cls = cls;
     ep.s = s ? s : stream;
@@ -307,9 +323,10 @@ struct Ctx {
   }
   void level_mark(int i) {  // 0 before a level's first launch, 1 after its join
     if (kernel_events) return;
-    if (!lvl_ev[i]) cudaEventCreate(&lvl_ev[i]);
-    cudaEventRecord(lvl_ev[i], stream);
-    lvl_open = true;
+    cudaEvent_t& e = lvl_ev_p[ev_par][i];
+    if (!e) cudaEventCreate(&e);
+    cudaEventRecord(e, stream);
+    lvl_open_p[ev_par] = true;
   }
   // after a stream sync: fold the pending event pairs into the per-class totals
   // level_ms = the wall span of the pending launches (first start to last end): a
@@ -317,8 +334,9 @@ struct Ctx {
   void collect_events(double* level_ms) {
     if (!kernel_events) {
       float ms = 0;
-      if (lvl_open && lvl_ev[0] && lvl_ev[1]) cudaEventElapsedTime(&ms, lvl_ev[0], lvl_ev[1]);
-      lvl_open = false;
+      cudaEvent_t* e = lvl_ev_p[ev_par];
+      if (lvl_open_p[ev_par] && e[0] && e[1]) cudaEventElapsedTime(&ms, e[0], e[1]);
+      lvl_open_p[ev_par] = false;
       if (level_ms) *level_ms = ms;
       return;
     }
@@ -450,6 +468,7 @@ void fill_params(Ctx* c, LevelParams& p) {
   p.dedup.table = c->table;
   p.dedup.mask = c->slots ? c->slots - 1 : 0;
   p.dedup.special = c->special;
+  p.out_base_dev = c->lag_prev_ctl ? c->d_lag_base + c->lag_par : nullptr;
   for (int q = 0; q < kMaxW32; ++q) { p.pos[q] = c->tab.pos[q]; p.neg[q] = c->tab.neg[q]; }
 }
 
@@ -1395,6 +1414,10 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     p.tent = c->mode == DEDUP_HASHIDX ? 0x80000000u : 0u;
   }
   if ((s = reset_ctl(c)) != REI_OK) return s;
+  if (c->lag_prev_ctl) {  // lagged: this level's arena base from the previous level's count
+    launch_next_base(c->lag_prev_ctl, c->lag_prev_begin, c->d_lag_base + c->lag_par, c->ctl, c->stream);
+    ++c->launches;
+  }
   // operand blocks -> device (one small H2D per level).  Concatenation blocks are
   // split by orientation (left or right operand sliced): one launch each.
   std::vector<Block> catv[2];
@@ -1451,10 +1474,11 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   // level (Q / S blocks); concatenation / union blocks wait only if one of them does
   if (c->post_pending) {
     bool binary_reads = conc < 1;
-    for (const Block& b : cat) binary_reads |= b.a_base == c->levels.at(c->post_level).begin ||
-                                               b.b_base == c->levels.at(c->post_level).begin;
-    for (const Block& b : uni) binary_reads |= b.a_base == c->levels.at(c->post_level).begin ||
-                                               b.b_base == c->levels.at(c->post_level).begin;
+    for (int pl : c->post_levels) {
+      const uint64_t pb = c->levels.at(pl).begin;
+      for (const Block& b : cat) binary_reads |= b.a_base == pb || b.b_base == pb;
+      for (const Block& b : uni) binary_reads |= b.a_base == pb || b.b_base == pb;
+    }
     if (binary_reads) c->join_post();
   }
   c->level_mark(0);
@@ -1538,6 +1562,187 @@ bool needs_uncached(const Ctx* c, int cost) {
 }
 
 // Algorithm 1 over all ranks of `g` (world = 1: the single-GPU path, no exchange).
+// ============================================================================
+// Lagged level loop (single rank).  A level that does not read the level launched just
+// before it -- its unary operands are levels c - c_opt, c - c_star and its binary
+// operands sum to c - c_cat / c - c_alt, so with unary costs > 1 (Table 1 row 8:
+// (10,10,10,1,10)) it never reads level c - 1 -- is planned and launched before that
+// level's count has come back: its arena base is computed on the device from the
+// previous level's count (k_next_base) and its control line alternates with the
+// previous one's.  At most two levels are in flight; a level is finalised (count,
+// precision, statistics, sort / transpose on the post stream) when a later level needs
+// it, or one level later.  The capacity for both is reserved up front (every candidate
+// new at worst); an overflow, a growth the budget refuses or an OnTheFly switch hands
+// the search back to the synchronous loop at that level.  A precise candidate in the
+// older level makes the younger one exit at once (k_next_base marks it) and the result
+// is the older level's.  REI_NO_LAG=1 turns it off.
+bool lag_ok(const Ctx* c) {
+  return !c->sharded && !c->otf_level && c->world == 1 && !c->exchange_self && !c->kernel_events &&
+         (c->mode == DEDUP_BITMAP || c->mode == DEDUP_HASH64) && c->W32 <= 2 &&
+         !(c->flags & REI_FLAG_COMPLETE_FINAL_LEVEL) && getenv("REI_NO_LAG") == nullptr;
+}
+
+rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* cand, bool* done) {
+  *done = false;
+  const rei_costs& k = c->costs;
+  const int c1 = (int)k.sym;
+  rei_status s;
+  if (!c->d_lag_base && c->dmalloc(&c->d_lag_base, 2 * sizeof(unsigned long long)) != cudaSuccess) return REI_OK;
+  if (!c->h_lag && host_alloc(reinterpret_cast<void**>(&c->h_lag), 2 * sizeof(LevelCtl)) != cudaSuccess) return REI_OK;
+  for (auto& e : c->ev_lag)
+    if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return REI_OK;
+  struct Fly {
+    int cost;
+    LevelInfo lv;
+    uint64_t nq, ns, ncat, nuni;
+    int par;
+  };
+  std::deque<Fly> fly;
+  std::vector<Block> cat, uni;
+  const bool trace = getenv("REI_TRACE") != nullptr;
+  auto reads = [&](int cost, int x) {
+    return cost - (int)k.opt == x || cost - (int)k.star == x || cost - (int)k.cat - x >= c1 ||
+           cost - (int)k.alt - x >= c1;
+  };
+  auto total = [](const Fly& f) { return f.nq + f.ns + f.ncat + f.nuni; };
+  // finalise the oldest level in flight; *stop: the search ended (found) or goes back
+  // to the synchronous loop (*first_cost set)
+  auto finalize = [&](bool* stop) -> rei_status {
+    Fly f = fly.front();
+    fly.pop_front();
+    CUDA_OK(c, cudaEventSynchronize(c->ev_lag[f.par]));
+    const LevelCtl ctl = c->h_lag[f.par];
+    c->d2h_bytes += sizeof(LevelCtl);
+    c->ev_par = f.par;
+    double ms = 0;
+    c->collect_events(&ms);
+    if (ctl.overflow) {  // redo from this level in the synchronous loop (younger levels exit at once)
+      CUDA_OK(c, cudaStreamSynchronize(c->stream));
+      fly.clear();
+      rei_status r = rebuild_dedup(c, c->arena_used);
+      *first_cost = f.cost;
+      *stop = true;
+      return r;
+    }
+    const bool found = ctl.found_rank != ~0ull;
+    f.lv.begin = c->arena_used;
+    f.lv.size = ctl.count;
+    f.lv.slab = c->slabs_used;
+    rei_level_stat st{};
+    st.cost = (uint32_t)f.cost;
+    st.cand_q = f.nq; st.cand_s = f.ns; st.cand_c = f.ncat; st.cand_u = f.nuni;
+    st.unique = f.lv.size;
+    st.ms = ms;
+    st.complete = found ? 0 : 1;
+    st.evaluated = found ? ctl.evaluated : total(f);
+    st.eval_c = found ? ctl.eval_c : f.ncat;
+    st.eval_u = found ? ctl.eval_u : f.nuni;
+    if (trace) fprintf(stderr, "[rei_solve] level %3d (lagged) device %8.3f ms\n", f.cost, ms);
+    c->levels[f.cost] = f.lv;
+    c->stats.push_back(st);
+    if (found) {
+      CUDA_OK(c, cudaStreamSynchronize(c->stream));  // the younger level saw the mark and exited
+      fly.clear();
+      c->arena_used = f.lv.begin + f.lv.size;
+      c->result.candidates = *cand + st.evaluated;
+      *stop = true;
+      *done = true;
+      return finish_found(c, f.cost, ctl.found_rank);
+    }
+    *cand += total(f);
+    c->result.cand_complete = *cand;
+    c->result.candidates = *cand;
+    c->result.last_complete_cost = (uint32_t)f.cost;
+    c->arena_used += f.lv.size;
+    // sort + transpose after this level's kernels only (younger levels never read it)
+    cudaStream_t ps = c->post ? c->post : c->stream;
+    if (c->post) CUDA_OK(c, cudaStreamWaitEvent(c->post, c->ev_lag[f.par], 0));
+    if (c->sort_levels && f.lv.size >= (1u << 14)) {
+      std::string err;
+      if (!sort_level((uint32_t)c->tab.n, c->arena + f.lv.begin, c->bp + f.lv.begin, f.lv.size, c->merge, ps, err,
+                      &c->launches, true)) {
+        c->err = err;
+        return REI_ECUDA;
+      }
+    }
+    EventPair et;
+    c->begin_kernel(REI_K_TRANSPOSE, et, ps);
+    const int n = launch_transpose(c->W32, c->arena, f.lv.begin, f.lv.size, c->tarena, f.lv.slab, ps);
+    c->end_kernel(et, n);
+    c->slabs_used += (f.lv.size + 31) / 32;
+    if (c->post) {
+      CUDA_OK(c, cudaEventRecord(c->ev_post, c->post));
+      c->post_pending = true;
+      c->post_level = f.cost;
+      c->post_levels.push_back(f.cost);
+    }
+    *stop = false;
+    return REI_OK;
+  };
+  auto drain = [&](bool* stop) -> rei_status {
+    *stop = false;
+    while (!fly.empty() && !*stop)
+      if ((s = finalize(stop)) != REI_OK) return s;
+    return REI_OK;
+  };
+  for (int cost = *first_cost; cost <= (int)max_cost; ++cost) {
+    bool stop = false;
+    // finalise what this level reads, and keep at most one level in flight under it
+    while (!fly.empty()) {
+      bool need = fly.size() >= 2;
+      for (const Fly& f : fly) need |= reads(cost, f.cost);
+      if (!need) break;
+      if ((s = finalize(&stop)) != REI_OK) return s;
+      if (stop) return REI_OK;
+    }
+    LevelInfo lv;
+    lv.cost = cost;
+    uint64_t nq, ns, ncat, nuni;
+    plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);
+    if (lv.plan.empty()) continue;
+    const uint64_t tot = nq + ns + ncat + nuni;
+    uint64_t infl = 0;
+    for (const Fly& f : fly) infl += total(f);
+    const uint64_t cap = c->entry_limit ? std::min<uint64_t>(c->cap, c->entry_limit) : c->cap;
+    if (!fly.empty() && (c->arena_used + infl + tot > cap || c->slabs_used + (infl + tot) / 32 + 4 > c->slab_cap)) {
+      if ((s = drain(&stop)) != REI_OK) return s;
+      if (stop) return REI_OK;
+    }
+    if (fly.empty()) {  // as the synchronous loop: grow ahead when the level may not fit
+      const uint64_t prev = c->stats.empty() ? 0 : c->stats.back().unique;
+      const uint64_t expect = std::min<uint64_t>(tot, 4 * prev + 1024);
+      if (c->arena_used + expect > c->cap || c->slabs_used + expect / 32 + 2 > c->slab_cap) {
+        if ((s = grow(c, c->arena_used + expect)) != REI_OK) {
+          if (s != REI_OUT_OF_MEMORY) return s;
+          *first_cost = cost;  // the synchronous loop handles OnTheFly
+          return REI_OK;
+        }
+      }
+    }
+    const int par = fly.empty() ? (c->lag_par ^ 1) : (fly.back().par ^ 1);
+    c->ctl = c->ctl_base + par;
+    c->ev_par = par;
+    if (!fly.empty()) {
+      c->lag_prev_ctl = c->ctl_base + fly.back().par;
+      c->lag_prev_begin = c->arena_used;  // every level before the one in flight is final
+    }
+    c->lag_par = par;
+    lv.begin = c->arena_used;  // final only when nothing is in flight
+    s = launch_level(c, 0, 1, cost, lv.begin, nq, ns, cat, uni, false);
+    c->lag_prev_ctl = nullptr;
+    if (s != REI_OK) return s;
+    CUDA_OK(c, cudaMemcpyAsync(c->h_lag + par, c->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OK(c, cudaEventRecord(c->ev_lag[par], c->stream));
+    fly.push_back({cost, lv, nq, ns, ncat, nuni, par});
+  }
+  bool stop = false;
+  if ((s = drain(&stop)) != REI_OK) return s;
+  if (!stop) *first_cost = (int)max_cost + 1;
+  c->ctl = c->ctl_base;
+  c->ev_par = 0;
+  return REI_OK;
+}
+
 rei_status solve_group(Comm& g, uint32_t max_cost) {
   Ctx* c0 = g.m[0];
   const rei_costs& k = c0->costs;
@@ -1617,6 +1822,13 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
   if (loop_ok) {
     bool done = false;
     if ((s = device_levels(c0, max_cost, c1 + 1, &first_cost, &cand, &done)) != REI_OK) return s;
+    if (done) return REI_OK;
+  }
+  if (!multi && g.m.size() == 1 && lag_ok(c0)) {
+    bool done = false;
+    if ((s = solve_lagged(c0, max_cost, &first_cost, &cand, &done)) != REI_OK) return s;
+    c0->ctl = c0->ctl_base;
+    c0->ev_par = 0;
     if (done) return REI_OK;
   }
   // REI_LOOP_RESUME=1: after a big level on the host, a run of small levels goes back to
@@ -1831,6 +2043,7 @@ rei_status solve_group(Comm& g, uint32_t max_cost) {
         CUDA_OK(c, cudaEventRecord(c->ev_post, c->post));
         c->post_pending = true;
         c->post_level = cost;
+        c->post_levels.push_back(cost);
       }
     }
   }

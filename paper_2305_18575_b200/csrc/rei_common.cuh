@@ -117,6 +117,10 @@ struct LevelParams {
   // (? count / arena base, * count / arena base / first slab) and of the transpose
   // (level count in un_q, arena base in un_bq, first slab in un_slab)
   uint64_t un_q, un_s, un_bq, un_bs, un_slab;
+  // lagged levels (rei_api.cu solve_group): the level's first arena index is computed on
+  // the device from the previous level's count (k_next_base) and read from here; null
+  // = out_base above
+  const unsigned long long* out_base_dev;
   uint32_t pos[kMaxW32];
   uint32_t neg[kMaxW32];
 };
