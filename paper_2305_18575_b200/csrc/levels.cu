@@ -2472,9 +2472,10 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
 // Lagged levels: the next level's first arena index = the previous (still unread) level's
 // first index + its count; a precise candidate or an overflow in that level makes the
 // next level's kernels exit at once (its found_rank is set; the host redoes or discards it)
-__global__ void k_next_base(const LevelCtl* __restrict__ prev, unsigned long long prev_begin,
+__global__ void k_next_base(const LevelCtl* __restrict__ prev, const unsigned long long* __restrict__ prev_base,
                             unsigned long long* __restrict__ base, LevelCtl* __restrict__ next) {
-  *base = prev_begin + prev->count;
+  *base = *prev_base + prev->count;
+  // a stop in the older level (precise candidate, overflow) -- or one passed down to it
   if (prev->found_rank != ~0ull || prev->overflow) next->found_rank = 0ull;
 }
 
@@ -2859,9 +2860,9 @@ int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const u
   REI_DISPATCH_W(W32, return launch_ops_t<W>(p, op, a, b, out, count, st));
 }
 
-int launch_next_base(const LevelCtl* prev, unsigned long long prev_begin, unsigned long long* base, LevelCtl* next,
-                     cudaStream_t st) {
-  k_next_base<<<1, 1, 0, st>>>(prev, prev_begin, base, next);
+int launch_next_base(const LevelCtl* prev, const unsigned long long* prev_base, unsigned long long* base,
+                     LevelCtl* next, cudaStream_t st) {
+  k_next_base<<<1, 1, 0, st>>>(prev, prev_base, base, next);
   return 1;
 }
 

@@ -208,12 +208,18 @@ struct Ctx {
   }
   // lagged levels (solve_lagged): device base of the level being launched, the previous
   // (unread) level's control line and first arena index
-  unsigned long long* d_lag_base = nullptr;  // [2]
+  static constexpr int kLag = 4;              // control-line slots: up to kLag - 1 levels in flight
+  unsigned long long* d_lag_base = nullptr;  // [kLag] device arena base of each slot's level
+  unsigned long long* h_lag_base = nullptr;  // pinned [kLag]: host-known bases copied to the device
   const LevelCtl* lag_prev_ctl = nullptr;
-  uint64_t lag_prev_begin = 0;
+  int lag_prev_par = 0;
   int lag_par = 0;
-  LevelCtl* h_lag = nullptr;  // pinned [2]: control lines read back without a stream sync
-  cudaEvent_t ev_lag[2] = {nullptr, nullptr};
+  LevelCtl* h_lag = nullptr;  // pinned [kLag]: control lines read back without a stream sync
+  // pinned block tables [kLag][3][kMaxBlocks]: a lagged level's H2D copy of its plan may
+  // run after the host has planned the next level, so each slot has its own staging
+  Block* h_blocks_ring = nullptr;
+  bool lag_active = false;
+  cudaEvent_t ev_lag[kLag] = {nullptr, nullptr, nullptr, nullptr};
 
   // multi-rank
   int world = 1, rank = 0;
@@ -268,6 +274,8 @@ struct Ctx {
     host_free(h_loop);
     host_free(h_rb);
     host_free(h_lag);
+    host_free(h_lag_base);
+    host_free(h_blocks_ring);
     for (auto e : ev_lag)
       if (e) cudaEventDestroy(e);
     host_free(h_peers);
@@ -303,8 +311,8 @@ struct Ctx {
   // per-kernel CUDA events (rei_kernel_stats); off (REI_KERNEL_EVENTS=0): one event
   // pair per level on the context's stream gives the level time
   bool kernel_events = false;  // on after rei_reset_kernel_stats (or REI_KERNEL_EVENTS=1)
-  cudaEvent_t lvl_ev_p[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  bool lvl_open_p[2] = {false, false};
+  cudaEvent_t lvl_ev_p[4][2] = {};
+  bool lvl_open_p[4] = {false, false, false, false};
   int ev_par = 0;  // which pair level_mark / collect_events use (lagged levels alternate)
   void begin_kernel(int cls, EventPair& ep, cudaStream_t s = nullptr) {
     ep.cls = cls;
@@ -1415,7 +1423,7 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   }
   if ((s = reset_ctl(c)) != REI_OK) return s;
   if (c->lag_prev_ctl) {  // lagged: this level's arena base from the previous level's count
-    launch_next_base(c->lag_prev_ctl, c->lag_prev_begin, c->d_lag_base + c->lag_par, c->ctl, c->stream);
+    launch_next_base(c->lag_prev_ctl, c->d_lag_base + c->lag_prev_par, c->d_lag_base + c->lag_par, c->ctl, c->stream);
     ++c->launches;
   }
   // operand blocks -> device (one small H2D per level).  Concatenation blocks are
@@ -1437,10 +1445,12 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
         return REI_EINVAL;
       }
   }
+  Block* hb = (c->lag_active && c->h_blocks_ring) ? c->h_blocks_ring + (size_t)c->lag_par * 3 * Ctx::kMaxBlocks
+                                                  : c->h_blocks;
   for (int r = 0; r < 3; ++r) {
     if (lists[r]->empty()) continue;
-    std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
-    CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, c->h_blocks + r * Ctx::kMaxBlocks,
+    std::copy(lists[r]->begin(), lists[r]->end(), hb + r * Ctx::kMaxBlocks);
+    CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, hb + r * Ctx::kMaxBlocks,
                                lists[r]->size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
     c->h2d_bytes += lists[r]->size() * sizeof(Block);
   }
@@ -1587,8 +1597,13 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
   const rei_costs& k = c->costs;
   const int c1 = (int)k.sym;
   rei_status s;
-  if (!c->d_lag_base && c->dmalloc(&c->d_lag_base, 2 * sizeof(unsigned long long)) != cudaSuccess) return REI_OK;
-  if (!c->h_lag && host_alloc(reinterpret_cast<void**>(&c->h_lag), 2 * sizeof(LevelCtl)) != cudaSuccess) return REI_OK;
+  constexpr int K = Ctx::kLag;
+  if (!c->d_lag_base && c->dmalloc(&c->d_lag_base, K * sizeof(unsigned long long)) != cudaSuccess) return REI_OK;
+  if (!c->h_lag && host_alloc(reinterpret_cast<void**>(&c->h_lag), K * sizeof(LevelCtl)) != cudaSuccess) return REI_OK;
+  if (!c->h_lag_base && host_alloc(reinterpret_cast<void**>(&c->h_lag_base), K * 8) != cudaSuccess) return REI_OK;
+  if (!c->h_blocks_ring && host_alloc(reinterpret_cast<void**>(&c->h_blocks_ring),
+                                      sizeof(Block) * K * 3 * Ctx::kMaxBlocks) != cudaSuccess)
+    return REI_OK;
   for (auto& e : c->ev_lag)
     if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return REI_OK;
   struct Fly {
@@ -1687,9 +1702,10 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
   };
   for (int cost = *first_cost; cost <= (int)max_cost; ++cost) {
     bool stop = false;
-    // finalise what this level reads, and keep at most one level in flight under it
+    // finalise what this level reads (and everything older), and keep at most K - 2
+    // levels in flight under it
     while (!fly.empty()) {
-      bool need = fly.size() >= 2;
+      bool need = fly.size() >= (size_t)(K - 1);
       for (const Fly& f : fly) need |= reads(cost, f.cost);
       if (!need) break;
       if ((s = finalize(&stop)) != REI_OK) return s;
@@ -1719,16 +1735,21 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
         }
       }
     }
-    const int par = fly.empty() ? (c->lag_par ^ 1) : (fly.back().par ^ 1);
+    const int par = (c->lag_par + 1) % K;  // round robin: in-order finalisation frees slots in order
     c->ctl = c->ctl_base + par;
     c->ev_par = par;
     if (!fly.empty()) {
       c->lag_prev_ctl = c->ctl_base + fly.back().par;
-      c->lag_prev_begin = c->arena_used;  // every level before the one in flight is final
+      c->lag_prev_par = fly.back().par;
+    } else {  // a host-known base, on the device for the next level to chain from
+      c->h_lag_base[par] = c->arena_used;
+      CUDA_OK(c, cudaMemcpyAsync(c->d_lag_base + par, c->h_lag_base + par, 8, cudaMemcpyHostToDevice, c->stream));
     }
     c->lag_par = par;
     lv.begin = c->arena_used;  // final only when nothing is in flight
+    c->lag_active = true;
     s = launch_level(c, 0, 1, cost, lv.begin, nq, ns, cat, uni, false);
+    c->lag_active = false;
     c->lag_prev_ctl = nullptr;
     if (s != REI_OK) return s;
     CUDA_OK(c, cudaMemcpyAsync(c->h_lag + par, c->ctl, sizeof(LevelCtl), cudaMemcpyDeviceToHost, c->stream));
@@ -2298,10 +2319,12 @@ rei_status launch_sharded(Ctx* c, int rank, int world, const std::vector<UnaryWo
         return REI_EINVAL;
       }
   }
+  Block* hb = (c->lag_active && c->h_blocks_ring) ? c->h_blocks_ring + (size_t)c->lag_par * 3 * Ctx::kMaxBlocks
+                                                  : c->h_blocks;
   for (int r = 0; r < 3; ++r) {
     if (lists[r]->empty()) continue;
-    std::copy(lists[r]->begin(), lists[r]->end(), c->h_blocks + r * Ctx::kMaxBlocks);
-    CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, c->h_blocks + r * Ctx::kMaxBlocks,
+    std::copy(lists[r]->begin(), lists[r]->end(), hb + r * Ctx::kMaxBlocks);
+    CUDA_OK(c, cudaMemcpyAsync(c->d_blocks + r * Ctx::kMaxBlocks, hb + r * Ctx::kMaxBlocks,
                                lists[r]->size() * sizeof(Block), cudaMemcpyHostToDevice, c->stream));
     c->h2d_bytes += lists[r]->size() * sizeof(Block);
   }
@@ -3084,7 +3107,7 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
       c->dmalloc(&c->tab.nsplit, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
       c->dmalloc(&c->tab.word_len, sizeof(uint32_t) * kMaxNW) != cudaSuccess ||
       c->dmalloc(&c->tab.seeds, sizeof(uint32_t) * kMaxW32 * k) != cudaSuccess ||
-      c->dmalloc(&c->ctl_base, 2 * sizeof(LevelCtl)) != cudaSuccess ||
+      c->dmalloc(&c->ctl_base, Ctx::kLag * sizeof(LevelCtl)) != cudaSuccess ||
       c->dmalloc(&c->d_peers, sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
       host_alloc(reinterpret_cast<void**>(&c->h_peers), sizeof(Peer) * Ctx::kMaxShards) != cudaSuccess ||
       c->dmalloc(&c->special, sizeof(unsigned int)) != cudaSuccess ||
