@@ -120,3 +120,43 @@ def test_device_loop_capacity_handover(monkeypatch):
     assert (rg.status, rg.last_complete_cost) == (ro.status, ro.last_complete_cost)
     if ro.status == "found":
         assert rg.cost == ro.cost and precise(rg.regex, sp.P, sp.N)
+
+
+# Lagged levels (rei_api.cu solve_lagged): with unary costs > 1 a level is launched
+# before the previous level's count is back.  The result must not depend on it.
+LAG_CASES = [
+    (specgen.TABLE1_ROW1.with_costs((10, 10, 10, 1, 10)), 150, {}),     # Table 1 row 8 costs
+    (specgen.C1_TOY.with_costs((2, 3, 3, 1, 2)), 30, {}),
+    (specgen.gen_type1("01", 4, 5, 5, 3, costs=(1, 2, 2, 1, 3)), 30, {}),
+    (specgen.gen_type2("01", 7, 6, 6, 0, costs=(2, 3, 3, 1, 2)), 30, {}),   # two-word CSs
+    (specgen.gen_type2("01", 7, 6, 6, 1, costs=(2, 3, 3, 1, 2)), 30, {"small_cache": True}),  # growth
+]
+
+
+@pytest.mark.parametrize("sp,K,kw", LAG_CASES, ids=[f"lag-{i}" for i in range(len(LAG_CASES))])
+def test_lagged_levels_equal_synchronous(sp, K, kw, monkeypatch):
+    gl, rl = solve(sp, K, monkeypatch, {"REI_NO_DEVICE_LOOP": "1"}, **kw)
+    gs, rs = solve(sp, K, monkeypatch, {"REI_NO_DEVICE_LOOP": "1", "REI_NO_LAG": "1"}, **kw)
+    assert (rl.status, rl.cost) == (rs.status, rs.cost)
+    ll, ls = levels_of(gl, rl), levels_of(gs, rs)
+    last = rl.cost if rl.status == "found" else K
+    for c in ls:
+        if c < last:
+            assert ll[c] == ls[c], c
+            assert sorted(gl.level_cs(c)) == sorted(gs.level_cs(c)), c
+    assert rl.cand_complete == rs.cand_complete
+    if rl.status == "found":
+        assert precise(rl.regex, sp.P, sp.N), rl.regex
+        assert re_cost(parse(rl.regex), sp.costs) == rl.cost
+
+
+def test_lagged_levels_vs_oracle(monkeypatch):
+    sp = specgen.gen_type1("01", 4, 5, 5, 3, costs=(1, 2, 2, 1, 3))
+    o = oracle.Oracle.from_spec(sp)
+    ro = o.solve(30)
+    g, rg = solve(sp, 30, monkeypatch, {"REI_NO_DEVICE_LOOP": "1"})
+    assert (rg.status, rg.cost) == (ro.status, ro.cost)
+    want = {l.cost: (l.unique, l.cand_q, l.cand_s, l.cand_c, l.cand_u) for l in ro.levels if l.complete}
+    for l in rg.levels:
+        if l.complete == 1 and l.cost in want:
+            assert (l.unique, l.cand_q, l.cand_s, l.cand_c, l.cand_u) == want[l.cost], l.cost
