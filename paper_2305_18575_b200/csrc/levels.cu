@@ -920,6 +920,11 @@ __global__ void __launch_bounds__(kWarps * 32) k_concat(LevelParams p) {
 
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  if (p.rank_off_dev) {  // split level: the ? / * candidates (ranked first) counted on the device
+    __syncthreads();
+    const unsigned long long off = __ldg(p.rank_off_dev);
+    for (int i = threadIdx.x; i < (int)p.nblocks; i += blockDim.x) s_blocks[i].cand_off += off;
+  }
   for (int i = threadIdx.x; i < (int)(p.maxk * NW); i += blockDim.x)
     s_split[i] = p.split[(i / NW) * kMaxNW + (i % NW)];
   for (int i = threadIdx.x; i < NW; i += blockDim.x) s_nsplit[i] = p.nsplit[i];
@@ -1109,6 +1114,11 @@ __global__ void __launch_bounds__(kWarps * 32, W == 4 ? REI_WIDE_MINB : REI_WIDE
   uint32_t* s_warp = s_cv + MAXK * NW;                                  // [kWarps][NW + G * MW]
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  if (p.rank_off_dev) {  // split level: the ? / * candidates (ranked first) counted on the device
+    __syncthreads();
+    const unsigned long long off = __ldg(p.rank_off_dev);
+    for (int i = threadIdx.x; i < (int)p.nblocks; i += blockDim.x) s_blocks[i].cand_off += off;
+  }
   for (int i = threadIdx.x; i < MAXK * NW; i += blockDim.x) {
     const uint32_t k = i / NW, w = i % NW;
     const bool ok = w < p.n && k < p.nsplit[w];
@@ -1288,6 +1298,11 @@ __device__ __forceinline__ void concat_fast_body(const LevelParams& p, uint32_t 
   uint32_t* s_src = reinterpret_cast<uint32_t*>(s_blocks + p.nblocks);  // [MAXK][NW]
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  if (p.rank_off_dev) {  // split level: the ? / * candidates (ranked first) counted on the device
+    __syncthreads();
+    const unsigned long long off = __ldg(p.rank_off_dev);
+    for (int i = threadIdx.x; i < (int)p.nblocks; i += blockDim.x) s_blocks[i].cand_off += off;
+  }
   // REVL (one-word CSs): lane l computes the slice of word 31 - l, so the transposed
   // candidate comes out bit-reversed -- its bitmap position is one shift away
 #ifdef REI_NO_REVLANES
@@ -1560,6 +1575,11 @@ __device__ __forceinline__ void union_body(const LevelParams& p, uint32_t bid, u
   Block* s_blocks = reinterpret_cast<Block*>(smem_raw);
   for (int i = threadIdx.x; i < (int)(p.nblocks * sizeof(Block) / 4); i += blockDim.x)
     reinterpret_cast<uint32_t*>(s_blocks)[i] = reinterpret_cast<const uint32_t*>(p.blocks)[i];
+  if (p.rank_off_dev) {  // split level: the ? / * candidates (ranked first) counted on the device
+    __syncthreads();
+    const unsigned long long off = __ldg(p.rank_off_dev);
+    for (int i = threadIdx.x; i < (int)p.nblocks; i += blockDim.x) s_blocks[i].cand_off += off;
+  }
   __syncthreads();
   const uint32_t lane = lane_id();
   const unsigned long long gwarp = (unsigned long long)bid * kWarps + (threadIdx.x >> 5);
@@ -2473,8 +2493,10 @@ __global__ void __launch_bounds__(256) k_level_loop(LevelParams p0, DevLoop d) {
 // first index + its count; a precise candidate or an overflow in that level makes the
 // next level's kernels exit at once (its found_rank is set; the host redoes or discards it)
 __global__ void k_next_base(const LevelCtl* __restrict__ prev, const unsigned long long* __restrict__ prev_base,
-                            unsigned long long* __restrict__ base, LevelCtl* __restrict__ next) {
+                            unsigned long long* __restrict__ base, LevelCtl* __restrict__ next,
+                            unsigned long long* __restrict__ rank_off, uint32_t unary_reads_prev) {
   *base = *prev_base + prev->count;
+  if (rank_off) *rank_off = prev->count * unary_reads_prev;  // ? and / or * operands of that level
   // a stop in the older level (precise candidate, overflow) -- or one passed down to it
   if (prev->found_rank != ~0ull || prev->overflow) next->found_rank = 0ull;
 }
@@ -2861,8 +2883,8 @@ int launch_ops(int W32, const LevelParams& p, int op, const uint32_t* a, const u
 }
 
 int launch_next_base(const LevelCtl* prev, const unsigned long long* prev_base, unsigned long long* base,
-                     LevelCtl* next, cudaStream_t st) {
-  k_next_base<<<1, 1, 0, st>>>(prev, prev_base, base, next);
+                     LevelCtl* next, unsigned long long* rank_off, uint32_t unary_reads_prev, cudaStream_t st) {
+  k_next_base<<<1, 1, 0, st>>>(prev, prev_base, base, next, rank_off, unary_reads_prev);
   return 1;
 }
 

@@ -219,6 +219,10 @@ struct Ctx {
   // run after the host has planned the next level, so each slot has its own staging
   Block* h_blocks_ring = nullptr;
   bool lag_active = false;
+  // split levels: part 1 = the binary kernels only (no join), part 2 = the unary kernel only
+  int lag_part = 0;
+  uint32_t lag_unary_reads = 0;          // how many of the level's ? / * sources are the level in flight
+  unsigned long long* d_rank_off = nullptr;  // [kLag]
   cudaEvent_t ev_lag[kLag] = {nullptr, nullptr, nullptr, nullptr};
 
   // multi-rank
@@ -269,7 +273,7 @@ struct Ctx {
     for (void* q : {(void*)arena, (void*)bp, (void*)tarena, (void*)bitmap, (void*)table, (void*)special,
                     (void*)ctl_base, (void*)d_blocks, (void*)d_peers, (void*)tab.split, (void*)tab.nsplit,
                     (void*)tab.word_len, (void*)tab.seeds, (void*)d_ctl_all, (void*)st_cs, (void*)st_bp,
-                    (void*)d_small, (void*)d_small_all, d_loop, (void*)d_lag_base})
+                    (void*)d_small, (void*)d_small_all, d_loop, (void*)d_lag_base, (void*)d_rank_off})
       dfree(q);
     host_free(h_loop);
     host_free(h_rb);
@@ -476,7 +480,8 @@ void fill_params(Ctx* c, LevelParams& p) {
   p.dedup.table = c->table;
   p.dedup.mask = c->slots ? c->slots - 1 : 0;
   p.dedup.special = c->special;
-  p.out_base_dev = c->lag_prev_ctl ? c->d_lag_base + c->lag_par : nullptr;
+  p.out_base_dev = (c->lag_prev_ctl || c->lag_part == 2) ? c->d_lag_base + c->lag_par : nullptr;
+  p.rank_off_dev = (c->lag_part == 1 && c->lag_unary_reads) ? c->d_rank_off + c->lag_par : nullptr;
   for (int q = 0; q < kMaxW32; ++q) { p.pos[q] = c->tab.pos[q]; p.neg[q] = c->tab.neg[q]; }
 }
 
@@ -1421,9 +1426,12 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     p.stage_cs = c->st_cs;
     p.tent = c->mode == DEDUP_HASHIDX ? 0x80000000u : 0u;
   }
-  if ((s = reset_ctl(c)) != REI_OK) return s;
-  if (c->lag_prev_ctl) {  // lagged: this level's arena base from the previous level's count
-    launch_next_base(c->lag_prev_ctl, c->d_lag_base + c->lag_prev_par, c->d_lag_base + c->lag_par, c->ctl, c->stream);
+  const int part = c->lag_part;  // 0 whole level, 1 binary kernels only, 2 unary kernel only
+  if (part != 2 && (s = reset_ctl(c)) != REI_OK) return s;
+  if (part != 2 && c->lag_prev_ctl) {  // lagged: this level's arena base from the previous level's count
+    launch_next_base(c->lag_prev_ctl, c->d_lag_base + c->lag_prev_par, c->d_lag_base + c->lag_par, c->ctl,
+                     part == 1 && c->lag_unary_reads ? c->d_rank_off + c->lag_par : nullptr, c->lag_unary_reads,
+                     c->stream);
     ++c->launches;
   }
   // operand blocks -> device (one small H2D per level).  Concatenation blocks are
@@ -1491,14 +1499,19 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
     }
     if (binary_reads) c->join_post();
   }
-  c->level_mark(0);
+  if (part != 2) c->level_mark(0);
   if (conc >= 1) {
-    CUDA_OK(c, cudaEventRecord(c->ev_fork, c->stream));
-    for (int i = 0; i < conc; ++i) CUDA_OK(c, cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0));
-    c->wait_post(su);  // su = aux[0]: the unary kernel
-    c->post_pending = false;  // the join below makes the context's stream wait for su
+    if (part != 2) {  // part 2 runs on the streams part 1 forked
+      CUDA_OK(c, cudaEventRecord(c->ev_fork, c->stream));
+      for (int i = 0; i < conc; ++i) CUDA_OK(c, cudaStreamWaitEvent(c->aux[i], c->ev_fork, 0));
+    }
+    if (part != 1) {
+      c->wait_post(su);  // su = aux[0]: the unary kernel
+      c->post_pending = false;  // the join below makes the context's stream wait for su
+      c->post_levels.clear();
+    }
   }
-  if (nq + ns) {
+  if (part != 1 && nq + ns) {
     const uint64_t bq = nq ? c->levels.at(cost - (int)k.opt).begin : 0;
     const uint64_t bs = ns ? c->levels.at(cost - (int)k.star).begin : 0;
     const uint64_t slab_s = ns ? c->levels.at(cost - (int)k.star).slab : 0;
@@ -1539,7 +1552,13 @@ rei_status launch_level(Ctx* c, int rank, int world, int cost, uint64_t begin, u
   };
   // union first (bitmap dedup default, REI_UNION_FIRST): the union kernel takes the SMs
   // first, so a precise union is met early at c* (see rei_init)
-  if (c->union_first) { launch_uni(); launch_cat(); } else { launch_cat(); launch_uni(); }
+  if (part != 2) {
+    if (c->union_first) { launch_uni(); launch_cat(); } else { launch_cat(); launch_uni(); }
+  }
+  if (part == 1) {  // split level: the unary part (part 2) joins the streams
+    CUDA_OK(c, cudaGetLastError());
+    return REI_OK;
+  }
   if (conc >= 1) {  // join
     for (int i = 0; i < conc; ++i) {
       CUDA_OK(c, cudaEventRecord(c->ev_join[i], c->aux[i]));
@@ -1604,6 +1623,8 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
   if (!c->h_blocks_ring && host_alloc(reinterpret_cast<void**>(&c->h_blocks_ring),
                                       sizeof(Block) * K * 3 * Ctx::kMaxBlocks) != cudaSuccess)
     return REI_OK;
+  if (!c->d_rank_off && c->dmalloc(&c->d_rank_off, K * sizeof(unsigned long long)) != cudaSuccess) return REI_OK;
+  const bool split_ok = getenv("REI_NO_SPLIT") == nullptr;
   for (auto& e : c->ev_lag)
     if (!e && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return REI_OK;
   struct Fly {
@@ -1702,9 +1723,15 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
   };
   for (int cost = *first_cost; cost <= (int)max_cost; ++cost) {
     bool stop = false;
+    // split level: when the only level in flight is read by this level's ? / * blocks
+    // alone, its binary kernels go first (they never read it) and the unary kernel
+    // follows once that level is final
+    auto binary_reads = [&](int x) { return cost - (int)k.cat - x >= c1 || cost - (int)k.alt - x >= c1; };
+    const bool split = split_ok && fly.size() == 1 && !binary_reads(fly.back().cost) &&
+                       (cost - (int)k.opt == fly.back().cost || cost - (int)k.star == fly.back().cost);
     // finalise what this level reads (and everything older), and keep at most K - 2
     // levels in flight under it
-    while (!fly.empty()) {
+    while (!split && !fly.empty()) {
       bool need = fly.size() >= (size_t)(K - 1);
       for (const Fly& f : fly) need |= reads(cost, f.cost);
       if (!need) break;
@@ -1715,14 +1742,21 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
     lv.cost = cost;
     uint64_t nq, ns, ncat, nuni;
     plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);
-    if (lv.plan.empty()) continue;
-    const uint64_t tot = nq + ns + ncat + nuni;
+    if (lv.plan.empty() && !split) continue;  // (split: the ? / * blocks of the level in flight)
+    uint64_t tot = nq + ns + ncat + nuni;
     uint64_t infl = 0;
     for (const Fly& f : fly) infl += total(f);
+    // a split level also has the ? / * candidates of the level in flight (<= 2 x its candidates)
+    const uint64_t need = tot + (split ? 2 * infl : 0);
     const uint64_t cap = c->entry_limit ? std::min<uint64_t>(c->cap, c->entry_limit) : c->cap;
-    if (!fly.empty() && (c->arena_used + infl + tot > cap || c->slabs_used + (infl + tot) / 32 + 4 > c->slab_cap)) {
+    if (!fly.empty() && (c->arena_used + infl + need > cap || c->slabs_used + (infl + need) / 32 + 4 > c->slab_cap)) {
       if ((s = drain(&stop)) != REI_OK) return s;
       if (stop) return REI_OK;
+      if (split) {  // the level in flight is final now: plan the whole level
+        plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);
+        tot = nq + ns + ncat + nuni;
+        if (lv.plan.empty()) continue;
+      }
     }
     if (fly.empty()) {  // as the synchronous loop: grow ahead when the level may not fit
       const uint64_t prev = c->stats.empty() ? 0 : c->stats.back().unique;
@@ -1748,7 +1782,35 @@ rei_status solve_lagged(Ctx* c, uint32_t max_cost, int* first_cost, uint64_t* ca
     c->lag_par = par;
     lv.begin = c->arena_used;  // final only when nothing is in flight
     c->lag_active = true;
-    s = launch_level(c, 0, 1, cost, lv.begin, nq, ns, cat, uni, false);
+    if (split && !fly.empty()) {
+      const int x = fly.back().cost;
+      c->lag_unary_reads = (cost - (int)k.opt == x ? 1u : 0u) + (cost - (int)k.star == x ? 1u : 0u);
+      c->lag_part = 1;  // binary kernels now (nq, ns of the level in flight counted on the device)
+      s = launch_level(c, 0, 1, cost, lv.begin, 0, 0, cat, uni, false);
+      c->lag_part = 0;
+      c->lag_prev_ctl = nullptr;
+      c->lag_active = false;
+      if (s != REI_OK) return s;
+      if ((s = finalize(&stop)) != REI_OK) return s;  // the level the unary blocks read
+      if (stop) return REI_OK;
+      plan_level(c, cost, lv, cat, uni, nq, ns, ncat, nuni);  // the full plan (ranks as the device's)
+      if (lv.plan.empty()) {  // the level in flight came back empty: no level at this cost
+        c->lag_unary_reads = 0;
+        continue;
+      }
+      lv.begin = c->arena_used;
+      c->ctl = c->ctl_base + par;
+      c->ev_par = par;
+      c->lag_par = par;
+      c->lag_part = 2;  // the unary kernel; appends from the device base of this level
+      c->lag_active = true;
+      std::vector<Block> none;
+      s = launch_level(c, 0, 1, cost, lv.begin, nq, ns, none, none, false);
+      c->lag_part = 0;
+      c->lag_unary_reads = 0;
+    } else {
+      s = launch_level(c, 0, 1, cost, lv.begin, nq, ns, cat, uni, false);
+    }
     c->lag_active = false;
     c->lag_prev_ctl = nullptr;
     if (s != REI_OK) return s;

@@ -121,6 +121,10 @@ struct LevelParams {
   // the device from the previous level's count (k_next_base) and read from here; null
   // = out_base above
   const unsigned long long* out_base_dev;
+  // split levels (solve_lagged): the binary kernels start before the count of the level
+  // their unary blocks read is back; that count (the ? / * candidates ranked first) is
+  // added to every block's cand_off on the device.  null = none
+  const unsigned long long* rank_off_dev;
   uint32_t pos[kMaxW32];
   uint32_t neg[kMaxW32];
 };

@@ -40,7 +40,7 @@ int launch_rehash(int W32, const LevelParams& p, uint64_t base, uint64_t count, 
 int launch_level_loop(int W32, const LevelParams& p, const DevLoop& d, cudaStream_t st);
 // Lagged levels: next level's arena base from the previous level's count (k_next_base).
 int launch_next_base(const LevelCtl* prev, const unsigned long long* prev_base, unsigned long long* base,
-                     LevelCtl* next, cudaStream_t st);
+                     LevelCtl* next, unsigned long long* rank_off, uint32_t unary_reads_prev, cudaStream_t st);
 // Packed launches (f4, rei_solve_packed): one grid, CTA group i runs pk.params[i]
 // (W32 in {1, 2} and <= 15 proper splits per word; maxk_class = 1, 3, 7 or 15).
 int packable(int W32, int maxk);
