@@ -95,3 +95,61 @@ def test_full_size_vs_oracle_golden(workload, stem):
         assert not prec.any(), c
         del arr
     g.close()
+
+
+# BASELINE configs[2] / [3] at throughput scale (1.2e10-1.5e10 candidates, 0.8e9-1.7e9
+# cached CSs: beyond the oracle's memory).  Checked by properties that hold at any size:
+# the planted target bounds c*; the returned regex is precise under `re` and costs
+# exactly c*; every complete level's candidate counts follow from the level sizes
+# (reading A9, Alg. 1 lines 5-8); sampled entries of deep levels reconstruct
+# to regexes denoting exactly their CS at exactly their cost; no cached CS
+# of those levels is precise (P11, P12).
+BIG = [("c3-big", "(0+1)*0(0+1)(0+1)(0+1)(0+1)"), ("c4-big", "(a+b+c)*d(a+c)(b+d)")]
+
+
+@pytest.mark.parametrize("workload,target", BIG, ids=[b[0] for b in BIG])
+def test_big_wide_properties(workload, target):
+    from paper_2305_18575_b200 import Solver
+    spec, max_cost, _ = bench.WORKLOADS[workload]
+    assert precise(target, spec.P, spec.N)  # the planting
+    g = Solver.from_spec(spec, device=0)
+    r = g.solve(max_cost)
+    assert r.status == "found"
+    assert r.cost <= re_cost(parse(target), spec.costs)
+    assert precise(r.regex, spec.P, spec.N), r.regex
+    assert re_cost(parse(r.regex), spec.costs) == r.cost
+    k_sym, k_opt, k_star, k_cat, k_alt = spec.costs
+    size = {l.cost: l.unique for l in r.levels}
+    for l in r.levels:
+        if l.complete != 1 or l.cost == k_sym:
+            continue
+        c = l.cost
+        assert l.cand_q == size.get(c - k_opt, 0) and l.cand_s == size.get(c - k_star, 0), c
+        cc = sum(size.get(a, 0) * size.get(c - k_cat - a, 0) for a in range(k_sym, c - k_cat - k_sym + 1))
+        cu = 0
+        for a in range(k_sym, c - k_alt + 1):
+            b = c - k_alt - a
+            if b < a:
+                break
+            cu += size.get(a, 0) * (size.get(a, 0) - 1) // 2 if a == b else size.get(a, 0) * size.get(b, 0)
+        assert (l.cand_c, l.cand_u) == (cc, cu), c
+    ic = g.ic()
+    idx = {w: i for i, w in enumerate(ic)}
+    W = r.cs_words
+    pm, nm = g.masks()
+    pw = np.array([(pm >> (32 * q)) & 0xFFFFFFFF for q in range(W)], dtype=np.uint32)
+    nw = np.array([(nm >> (32 * q)) & 0xFFFFFFFF for q in range(W)], dtype=np.uint32)
+    rng = random.Random(9)
+    deep = [l.cost for l in r.levels if l.complete == 1 and 0 < l.unique <= 4_000_000][-3:]
+    assert deep
+    for c in deep:
+        arr = g.level_cs_array(c)
+        for i in rng.sample(range(arr.shape[0]), min(15, arr.shape[0])):
+            rx = g.entry_regex(c, i)
+            cs_i = sum(int(arr[i, q]) << (32 * q) for q in range(W))
+            assert sum(1 << idx[w] for w in language_on(rx, ic)) == cs_i, (c, i, rx)
+            assert re_cost(parse(rx), spec.costs) == c
+        prec = np.all((arr & pw) == pw, axis=1) & np.all((arr & nw) == 0, axis=1)
+        assert not prec.any(), c
+        del arr
+    g.close()
