@@ -3184,7 +3184,14 @@ rei_status rei_init(void** out, const char* alphabet, const char* const* P, size
     ncclUniqueId id;
     memcpy(&id, opts->nccl_unique_id, sizeof(id));
     ncclComm_t comm;
-    if (!nccl_api().ok || nccl_api().CommInitRank(&comm, c->world, id, c->rank) != ncclSuccess) {
+    if (!nccl_api().ok) {
+      g_init_error = "NCCL not available";
+      return REI_ENCCL;
+    }
+    // NCCL allocates its own device buffers: hand the pool's idle blocks back first (a
+    // process that just ran a large search may hold tens of GB of them)
+    release_cached_memory();
+    if (nccl_api().CommInitRank(&comm, c->world, id, c->rank) != ncclSuccess) {
       g_init_error = "ncclCommInitRank failed";
       return REI_ENCCL;
     }

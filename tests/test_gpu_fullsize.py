@@ -95,6 +95,10 @@ def test_full_size_vs_oracle_golden(workload, stem):
         assert not prec.any(), c
         del arr
     g.close()
+    # tens of GB stay in the library's device pool otherwise: give them back to the
+    # driver so that later tests in this process (NCCL buffers, torch) can allocate
+    from paper_2305_18575_b200.rei import release_cached_memory
+    release_cached_memory()
 
 
 # BASELINE configs[2] / [3] at throughput scale (1.2e10-1.5e10 candidates, 0.8e9-1.7e9
@@ -153,3 +157,7 @@ def test_big_wide_properties(workload, target):
         assert not prec.any(), c
         del arr
     g.close()
+    # tens of GB stay in the library's device pool otherwise: give them back to the
+    # driver so that later tests in this process (NCCL buffers, torch) can allocate
+    from paper_2305_18575_b200.rei import release_cached_memory
+    release_cached_memory()
