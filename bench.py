@@ -276,9 +276,12 @@ def roofline_of(kstats, kresults, kstep_ms, ic_words, w32, world, kernel_pass, w
     tpath = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get(workload, {}).get(dom)
+    traffic_note = ("DRAM bytes (read + write) of the longest launch of this kernel in one ncu --set full "
+                    "capture (profiles/roofline_traffic.json)") if traffic else None
     roof = {
         "bound": "alu", "achieved": achieved / 1e12, "peak": alu_peak / 1e12, "unit": "Tops/s",
         "frac": achieved / alu_peak, "frac_issue": achieved / issue_peak, "traffic": traffic,
+        "traffic_note": traffic_note,
         "kernel": f"k_{dom}<W32={w32}>", "ops_per_candidate": opc, "candidates_per_s": per_s,
         "launches": dom_launches, "avg_launch_ms": dom_ms / max(1, dom_launches),
         "share_of_step": dom_ms / sum(kstep_ms) if world == 1 and kstep_ms else None,
